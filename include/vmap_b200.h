@@ -1,0 +1,211 @@
+/*
+ * vmap_b200.h -- C ABI of the B200-native vMAP object-mapping step.
+ *
+ * The reference (`vobj`, /root/reference/pkg/src/vobj) is a pure-Python
+ * package; its "operator API" is the set of module-level functions its
+ * trainer calls.  Each entry point below replaces one of them and keeps its
+ * argument meaning and error behaviour (the Python mirror in
+ * paper_2302_01838_b200/ raises the same exception types from the codes).
+ *
+ * Conventions
+ *   - Every pointer is a DEVICE pointer owned by the caller (torch tensors in
+ *     the Python host); nothing is allocated inside except where a call says
+ *     so.  `stream` is a cudaStream_t passed as void*.
+ *   - Calls are asynchronous on `stream`; device-side failures (non-finite
+ *     gradients) are reported through a caller-provided device status word.
+ *   - Return codes: VM_OK, VM_ERR_SHAPE (bad arguments), VM_ERR_CUDA (launch
+ *     error; see vm_last_error()), VM_ERR_UNSUPPORTED (arch outside the
+ *     compiled kernel set).
+ *   - Not reentrant per stack (single writer).
+ *
+ * Parameter storage: one model-major arena per stack,
+ *   arena[capacity][block],  block = sum over layers of (fo_pad*fi_pad + fo_pad)
+ * with layer l's weight matrix at w_off[l] (row-major [fo_pad][fi_pad]) and
+ * its bias at b_off[l].  Padded rows/columns are zero and stay zero.  The
+ * reference's per-layer views `weights[l]: [capacity, fo, fi]`
+ * (models.py:69-71) are strided views of this arena.
+ */
+#ifndef VMAP_B200_H
+#define VMAP_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VM_OK 0
+#define VM_ERR_SHAPE 1
+#define VM_ERR_CUDA 3
+#define VM_ERR_UNSUPPORTED 4
+
+#define VM_MAX_LAYERS 8
+#define VM_MAX_STACKS 4
+
+/* models.py:19-55 ModelArch (output_dim is always 4: occupancy + RGB). */
+typedef struct VmArch {
+  int32_t n_layers;   /* >= 2 */
+  int32_t hidden;     /* 1..128 */
+  int32_t input_dim;  /* 3*include_input + 6*n_freq, 1..60 */
+  int32_t reserved;
+} VmArch;
+
+/* Arena layout of one model block, filled by vm_model_layout(). */
+typedef struct VmLayout {
+  int32_t n_layers;
+  int32_t hidden_pad;                 /* 32, 64 or 128 */
+  int32_t fo[VM_MAX_LAYERS], fi[VM_MAX_LAYERS];         /* true dims */
+  int32_t fo_pad[VM_MAX_LAYERS], fi_pad[VM_MAX_LAYERS]; /* arena dims */
+  int64_t w_off[VM_MAX_LAYERS], b_off[VM_MAX_LAYERS];   /* float offsets */
+  int64_t block;                      /* floats per model */
+  int64_t n_params;                   /* true parameter count per model */
+} VmLayout;
+
+/* StackedModelParams + OptimState (models.py:58-126). */
+typedef struct VmStack {
+  VmArch arch;
+  int32_t count;          /* live models K */
+  int32_t capacity;
+  float* params;          /* [capacity*block] */
+  float* m;               /* Adam first moment, same layout */
+  float* v;               /* Adam second moment */
+  int64_t* step;          /* [capacity] Adam step counters */
+  const uint8_t* frozen;  /* [capacity] */
+  /* Bias corrections f32(1 - beta^t) computed in f64 on the host exactly as
+     models.py:434-436 does; index t-1.  For t > corr_len both are 1.0f. */
+  const float* corr1;
+  const float* corr2;
+  int32_t corr_len;
+  /* f32 constants as numpy forms them (models.py:444-457):
+     beta1f = f32(b1), omb1 = f32(1-b1), beta2f, omb2 = f32(1-b2), eps, lr. */
+  float beta1f, omb1, beta2f, omb2, eps, lr;
+} VmStack;
+
+/* RaySampleBatch (trainer.py:162-173), stacked on a leading model axis.
+   Either `encoded` [K,R,S,D] (reference layout) or `points` [K,R,S,3]
+   (box-normalised sample points; positional encoding fused in-kernel with
+   `pe_scale` [K]) must be given. */
+typedef struct VmBatch {
+  int32_t n_models, n_rays, n_points, input_dim;
+  const float* encoded;
+  const float* points;
+  const float* pe_scale;
+  const float* t;              /* [K,R,S] */
+  const float* target_depth;   /* [K,R] */
+  const float* target_colour;  /* [K,R,3] */
+  const uint8_t* target_mask;  /* [K,R] */
+  const uint8_t* valid_depth;  /* [K,R] */
+  const uint8_t* ray_ok;       /* [K,R] */
+} VmBatch;
+
+/* LossWeights (render.py:61-64). */
+typedef struct VmLossWeights { float colour, occupancy; } VmLossWeights;
+
+/* Status words written by vm_train_step (device int32[4*n_stacks], caller
+   zero-fills nothing: the call initialises them):
+   [4s+0] first model index with a non-finite gradient among the models Adam
+          would update, or -1      (models.py:423-428 FloatingPointError)
+   [4s+1] first model index with a non-finite loss, or -1 (trainer.py:404-407)
+   [4s+2] 1 if Adam ran for stack s, else 0
+   [4s+3] reserved */
+
+/* ---- layout ---------------------------------------------------------- */
+int vm_model_layout(const VmArch* arch, VmLayout* out);
+
+/* ---- fused training step: replaces trainer.py:480-506 train_on_batch for
+   1..VM_MAX_STACKS stacks in one launch sequence (Mapper.train_step runs the
+   object stack then the background stack, trainer.py:364-390).  Stack s is
+   skipped (no Adam) when an earlier stack reported a non-finite gradient or
+   loss, matching the reference's raise-before-next-stack order. ----------- */
+size_t vm_train_workspace_bytes(const VmStack* stacks, const VmBatch* batches, int n_stacks);
+int vm_train_step(const VmStack* stacks, const VmBatch* batches, int n_stacks,
+                  VmLossWeights weights, float* losses /* [sum K][3] */,
+                  int32_t* status /* device [4*n_stacks] */,
+                  void* workspace, size_t workspace_bytes, void* stream);
+
+/* ---- models.py:311-355 forward: occupancy/colour for N samples per model.
+   encoded [K,N,D] -> occ [K,N], col [K,N,3]. -------------------------------- */
+int vm_forward(const VmStack* st, const float* encoded, int64_t n_samples,
+               float* occ, float* col, void* stream);
+
+/* ---- models.py:358-398 backward: parameter gradients given output grads.
+   Recomputes the forward from `encoded` (the activation cache is the input).
+   grads: [K][block] arena layout. ------------------------------------------- */
+int vm_backward(const VmStack* st, const float* encoded, int64_t n_samples,
+                const float* grad_occ, const float* grad_col, float* grads, void* stream);
+
+/* ---- models.py:401-467 adam_step over the stacked arena.  update_mask may be
+   NULL.  status: device int32[1], set to the first active model index with a
+   non-finite gradient (and then NOTHING is updated), else -1. --------------- */
+int vm_adam(const VmStack* st, const float* grads, const uint8_t* update_mask,
+            int32_t* status, void* stream);
+
+/* ---- render.py:230-281 occupancy rendering (bit-exact f32 op order). ------ */
+int vm_render_forward(int64_t n_rays, int32_t n_points, const float* occ, const float* col,
+                      const float* t, float* opacity, float* depth, float* colour,
+                      float* weights, float* trans, void* stream);
+int vm_render_backward(int64_t n_rays, int32_t n_points, const float* occ, const float* col,
+                       const float* t, const float* weights, const float* trans,
+                       const float* grad_opacity, const float* grad_depth,
+                       const float* grad_colour, float* d_occ, float* d_col, void* stream);
+/* ---- render.py:284-333 L1 losses (pairwise-summed over rays) and grads. --- */
+int vm_losses(int32_t n_models, int32_t n_rays, const float* opacity, const float* depth,
+              const float* colour, const float* target_depth, const float* target_colour,
+              const uint8_t* target_mask, const uint8_t* valid_depth, const uint8_t* ray_ok,
+              VmLossWeights w, float* l_depth, float* l_colour, float* l_occ, float* l_total,
+              float* grad_opacity, float* grad_depth, float* grad_colour, void* stream);
+
+/* ---- sampler: objects.py:323-352 + trainer.py:269-318 + render.py:76-227 --- */
+/* Keyframe crop texels live in one arena: texel (u,v) of keyframe j is
+   rgbd[kf.texel_off + (v-v0)*(u1-u0) + (u-u0)] (float4: r,g,b,depth z) and
+   mask[kf.texel_off + same] (uint8). */
+typedef struct VmKeyframe {
+  int64_t texel_off;
+  int32_t u0, v0, u1, v1;      /* half-open bbox in image pixels */
+  double pose[12];             /* camera-to-world rows 0..2 of the 4x4 */
+} VmKeyframe;
+
+typedef struct VmSampleObject {
+  int64_t object_id;           /* RNG key part (objects.py:335, trainer.py:304) */
+  int32_t kf_begin, n_kf;      /* keyframes [kf_begin, kf_begin+n_kf) */
+  int32_t active;              /* 0 -> zero batch (trainer.py:272-273, :336-338) */
+  int32_t reserved;
+  double box_min[3], box_max[3];   /* padded AABB (geometry.py:40-42) */
+  double center[3], half[3];       /* of the padded AABB */
+  double pe_scale;
+} VmSampleObject;
+
+typedef struct VmSampleParams {
+  uint64_t seed;
+  int64_t step;
+  int32_t n_rays, n_stratified, n_surface, encode; /* encode: 1 -> write encoded, 0 -> points */
+  int32_t n_freq, include_input, reserved0, reserved1;
+  double fx, fy, cx, cy;
+  int32_t width, height;
+  double t_near, t_far, surface_std, three_std; /* three_std = 3.0*surface_std (python f64) */
+} VmSampleParams;
+
+/* Debug/parity outputs of the sampler (optional, may be NULL). */
+typedef struct VmSampleAux {
+  int64_t* kf_idx; int64_t* u; int64_t* v;    /* [K,R] */
+  double* t64;                                 /* [K,R,S] f64 sorted samples */
+} VmSampleAux;
+
+size_t vm_sample_workspace_bytes(int n_objects, const VmSampleParams* p);
+int vm_sample(const VmSampleObject* objects /* device [K] */, int n_objects,
+              const VmKeyframe* keyframes /* device */, const float* rgbd /* float4 texels */,
+              const uint8_t* mask, const VmSampleParams* params, VmBatch* out /* device ptrs */,
+              VmSampleAux* aux, void* workspace, size_t workspace_bytes, void* stream);
+
+/* ---- misc ---------------------------------------------------------------- */
+const char* vm_last_error(void);
+const char* vm_version(void);
+/* FP32 FFMA throughput probe (roofline denominator): returns achieved
+   TFLOP/s measured with events around `iters` dependent-chain FFMAs. */
+int vm_ffma_peak(int iters, float* tflops, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VMAP_B200_H */

@@ -1,0 +1,546 @@
+"""CPU oracle for vMAP's vectorised object-mapping step -- TEST INFRASTRUCTURE ONLY.
+
+This module is a from-scratch numpy restatement of the reference `vobj`
+package's hot path (`/root/reference/pkg/src/vobj`).  It exists so that the
+CUDA implementation in `paper_2302_01838_b200` can be checked on identical
+seeded inputs.  Only `tests/`, `__graft_entry__.smoke()` and the
+`cpu_baseline` / `--impl reference` legs of `bench.py` may import it; the
+product path never does (it fails loudly without its CUDA library).
+
+Parity pinning: every function here is checked against golden vectors that
+`tests/golden/make_golden.py` produced by running the real reference in the
+build container (`tests/test_oracle_golden.py`).  Integer/RNG outputs and all
+f64 geometry are compared bit-exactly; BLAS-backed f32 matmul results are
+compared bit-exactly on the host that produced the goldens and to 1e-6
+elsewhere (OpenBLAS kernels differ per CPU).
+
+Each function cites the reference `file:line` whose arithmetic it restates.
+Operation order is deliberately the same as the reference's numpy expression
+order, because f32 results depend on it.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+from scipy.special import expit
+
+# Purpose codes, rng.py:15-21 (part of the replay contract).
+INIT_OBJECT, INIT_BACKGROUND, PIXELS, SAMPLES, BENCH = 1, 2, 3, 4, 5
+
+
+def keyed_rng(seed: int, purpose: int, *extra: int) -> np.random.Generator:
+    """rng.py:24-34 -- numpy Generator(PCG64(SeedSequence(key)))."""
+    key = (seed, purpose) + tuple(extra)
+    if any(k < 0 for k in key):
+        raise ValueError(f"rng key parts must be non-negative, got {key}")
+    return np.random.Generator(np.random.PCG64(np.random.SeedSequence(key)))
+
+
+# --------------------------------------------------------------------------
+# model stacks (models.py)
+# --------------------------------------------------------------------------
+
+@dataclass(frozen=True)
+class Arch:
+    """models.py:19-55."""
+    n_layers: int = 4
+    hidden: int = 32
+    n_freq: int = 5
+    include_input: bool = True
+
+    @property
+    def input_dim(self) -> int:
+        return 6 * self.n_freq + (3 if self.include_input else 0)
+
+    def dims(self) -> list[tuple[int, int]]:
+        """(fan_out, fan_in) first to last -- models.py:50-55."""
+        h = self.hidden
+        return [(h, self.input_dim)] + [(h, h)] * (self.n_layers - 2) + [(4, h)]
+
+
+@dataclass
+class Stack:
+    """Params + Adam state of K models (models.py:58-126)."""
+    arch: Arch
+    count: int
+    W: list
+    b: list
+    frozen: np.ndarray
+    mW: list
+    vW: list
+    mb: list
+    vb: list
+    step: np.ndarray
+    lr: float = 1e-3
+    beta1: float = 0.9
+    beta2: float = 0.999
+    eps: float = 1e-8
+
+    def copy(self) -> "Stack":
+        c = lambda xs: [x.copy() for x in xs]
+        return Stack(self.arch, self.count, c(self.W), c(self.b), self.frozen.copy(),
+                     c(self.mW), c(self.vW), c(self.mb), c(self.vb), self.step.copy(),
+                     self.lr, self.beta1, self.beta2, self.eps)
+
+
+def init_model_arrays(arch: Arch, seed: int, model_index: int, stream: int, dtype=np.float32):
+    """models.py:159-174: U(-1/sqrt(fi), 1/sqrt(fi)) weights then bias, per layer."""
+    g = keyed_rng(seed, stream, model_index)
+    ws, bs = [], []
+    for fo, fi in arch.dims():
+        lim = 1.0 / np.sqrt(fi)
+        ws.append(g.uniform(-lim, lim, size=(fo, fi)).astype(dtype))
+        bs.append(g.uniform(-lim, lim, size=fo).astype(dtype))
+    return ws, bs
+
+
+def new_stack(arch: Arch, count: int, seed: int, stream: int = INIT_OBJECT, dtype=np.float32,
+              lr=1e-3, beta1=0.9, beta2=0.999, eps=1e-8) -> Stack:
+    """init_stacked, models.py:199-219 (capacity = next power of two)."""
+    cap = max(1, int(2 ** np.ceil(np.log2(max(count, 1)))))
+    W = [np.zeros((cap, fo, fi), dtype) for fo, fi in arch.dims()]
+    b = [np.zeros((cap, fo), dtype) for fo, _ in arch.dims()]
+    st = Stack(arch, 0, W, b, np.zeros(cap, bool),
+               [np.zeros_like(x) for x in W], [np.zeros_like(x) for x in W],
+               [np.zeros_like(x) for x in b], [np.zeros_like(x) for x in b],
+               np.zeros(cap, np.int64), lr, beta1, beta2, eps)
+    for i in range(count):
+        ws, bs = init_model_arrays(arch, seed, i, stream, dtype)
+        for l in range(len(ws)):
+            st.W[l][i] = ws[l]
+            st.b[l][i] = bs[l]
+    st.count = count
+    return st
+
+
+def append(st: Stack, seed: int, stream: int = INIT_OBJECT) -> int:
+    """append_model, models.py:229-277 (grow to next pow2, init slot `count`)."""
+    k = st.count
+    if k + 1 > len(st.frozen):
+        cap = max(1, int(2 ** np.ceil(np.log2(k + 1))))
+        def grow(a):
+            out = np.zeros((cap,) + a.shape[1:], a.dtype)
+            out[:k] = a[:k]
+            return out
+        for name in ("W", "b", "mW", "vW", "mb", "vb"):
+            setattr(st, name, [grow(a) for a in getattr(st, name)])
+        st.frozen = grow(st.frozen)
+        st.step = grow(st.step)
+    ws, bs = init_model_arrays(st.arch, seed, k, stream, st.W[0].dtype)
+    for l in range(len(ws)):
+        st.W[l][k], st.b[l][k] = ws[l], bs[l]
+        for arr in (st.mW, st.vW):
+            arr[l][k] = 0
+        for arr in (st.mb, st.vb):
+            arr[l][k] = 0
+    st.step[k] = 0
+    st.frozen[k] = False
+    st.count = k + 1
+    return k
+
+
+def positional_encode(points, center, half, arch: Arch, scale: float) -> np.ndarray:
+    """models.py:286-308: p=(x-c)/h ; [p, sin(pi 2^i p/s), cos(...)] per band."""
+    x = np.asarray(points)
+    c = np.asarray(center, dtype=x.dtype)
+    h = np.asarray(half, dtype=x.dtype)
+    if np.any(h <= 0):
+        raise ValueError(f"half_extent must be positive, got {h}")
+    if scale <= 0:
+        raise ValueError(f"scale must be positive, got {scale}")
+    p = (x - c) / h
+    feats = [p] if arch.include_input else []
+    for band in range(arch.n_freq):
+        a = (np.pi * (2.0 ** band) / scale) * p
+        feats += [np.sin(a), np.cos(a)]
+    return np.concatenate(feats, axis=-1)
+
+
+def mlp_forward(st: Stack, enc: np.ndarray):
+    """models.py:311-355.  Returns (occ [K,N], col [K,N,3], inputs, masks)."""
+    k = st.count
+    x = np.ascontiguousarray(enc.reshape(k, -1, enc.shape[-1]))
+    inputs, masks = [], []
+    last = len(st.W) - 1
+    for l in range(last + 1):
+        inputs.append(x)
+        z = np.matmul(x, st.W[l][:k].transpose(0, 2, 1))
+        z += st.b[l][:k][:, None, :]
+        if l == last:
+            x = z
+        else:
+            masks.append(z > 0)
+            x = np.maximum(z, 0.0, out=z)
+    return expit(x[..., 0]), expit(x[..., 1:]), inputs, masks
+
+
+def mlp_backward(st: Stack, occ, col, inputs, masks, g_occ, g_col):
+    """models.py:358-398: sigmoid heads, then per layer dW=dz^T x, db=1^T dz, dx=dz W."""
+    k, n = occ.shape
+    dz = np.empty((k, n, 4), dtype=occ.dtype)
+    dz[..., 0] = np.asarray(g_occ).reshape(k, n) * occ * (1.0 - occ)
+    dz[..., 1:] = np.asarray(g_col).reshape(k, n, 3) * col * (1.0 - col)
+    ones = np.ones((1, 1, n), dtype=dz.dtype)
+    dW = [None] * len(st.W)
+    db = [None] * len(st.W)
+    for l in reversed(range(len(st.W))):
+        dW[l] = np.matmul(dz.transpose(0, 2, 1), inputs[l])
+        db[l] = np.matmul(ones, dz)[:, 0, :]
+        if l:
+            nxt = np.matmul(dz, st.W[l][:k])
+            nxt *= masks[l - 1]
+            dz = nxt
+    return dW, db
+
+
+def adam_update(st: Stack, dW, db, update_mask=None) -> None:
+    """models.py:401-467, op-for-op (f32 with f64 bias corrections)."""
+    k = st.count
+    act = ~st.frozen[:k]
+    if update_mask is not None:
+        act = act & np.asarray(update_mask, bool).reshape(k)
+    sel = np.flatnonzero(act)
+    if sel.size == 0:
+        return
+    bad = np.zeros(k, bool)
+    for gw, gb in zip(dW, db):
+        bad |= ~np.isfinite(gw).all(axis=(1, 2)) | ~np.isfinite(gb).all(axis=1)
+    bad &= act
+    if bad.any():
+        raise FloatingPointError(f"non-finite gradient for model index {int(np.flatnonzero(bad)[0])}")
+    dt = st.W[0].dtype
+    b1, b2 = st.beta1, st.beta2
+    tt = (st.step[sel] + 1).astype(np.float64)
+    c1 = (1.0 - b1 ** tt).astype(dt)
+    c2 = (1.0 - b2 ** tt).astype(dt)
+    lr = dt.type(st.lr)
+    every = sel.size == k
+
+    def one(p, m_all, v_all, g_all, shape):
+        g = g_all if every else g_all[sel]
+        m = m_all[:k] if every else m_all[sel]
+        v = v_all[:k] if every else v_all[sel]
+        m *= b1
+        m += (1.0 - b1) * g
+        g2 = np.square(g)
+        g2 *= 1.0 - b2
+        v *= b2
+        v += g2
+        if not every:
+            m_all[sel] = m
+            v_all[sel] = v
+        den = np.sqrt(v / c2.reshape(shape))
+        den += st.eps
+        upd = m / c1.reshape(shape)
+        upd /= den
+        upd *= lr
+        if every:
+            p[:k] -= upd
+        else:
+            p[sel] -= upd
+
+    for l in range(len(st.W)):
+        one(st.W[l], st.mW[l], st.vW[l], dW[l], (-1, 1, 1))
+        one(st.b[l], st.mb[l], st.vb[l], db[l], (-1, 1))
+    st.step[sel] += 1
+
+
+# --------------------------------------------------------------------------
+# rendering and losses (render.py)
+# --------------------------------------------------------------------------
+
+def render_forward(occ, col, t):
+    """render.py:230-246 -> (opacity, depth, colour, weights, trans)."""
+    occ = np.asarray(occ)
+    om = 1.0 - occ
+    T = np.empty_like(om)
+    T[..., 0] = 1.0
+    np.cumprod(om[..., :-1], axis=-1, out=T[..., 1:])
+    w = occ * T
+    return w.sum(axis=-1), (w * t).sum(axis=-1), (w[..., None] * col).sum(axis=-2), w, T
+
+
+def render_backward(occ, col, t, w, T, dO, dD, dC):
+    """render.py:249-281."""
+    g = dO[..., None] + dD[..., None] * t + (dC[..., None, :] * col).sum(axis=-1)
+    d_col = w[..., None] * dC[..., None, :]
+    gw = g * w
+    rev = np.flip(np.cumsum(np.flip(gw, axis=-1), axis=-1), axis=-1)
+    d_occ = g * T - (rev - gw) / np.maximum(1.0 - occ, 1e-7)
+    return d_occ, d_col
+
+
+def _loss_masks(mask, valid, ok, dtype):
+    mask = np.asarray(mask, bool)
+    m_ok = mask & ok
+    return (mask.astype(dtype), (m_ok & valid).astype(dtype), m_ok.astype(dtype),
+            np.asarray(ok, bool).astype(dtype))
+
+
+def losses(O, D, C, tgt_d, tgt_c, mask, valid, ok, w_colour=5.0, w_occ=10.0):
+    """render.py:284-309 -> (L_depth, L_colour, L_occ, total) summed over rays."""
+    m_ind, wd, wc, wo = _loss_masks(mask, valid, ok, D.dtype)
+    ld = (wd * np.abs(D - tgt_d)).sum(axis=-1)
+    lc = (wc * np.abs(C - tgt_c).sum(axis=-1)).sum(axis=-1)
+    lo = (wo * np.abs(O - m_ind)).sum(axis=-1)
+    return ld, lc, lo, ld + w_colour * lc + w_occ * lo
+
+
+def loss_grads(O, D, C, tgt_d, tgt_c, mask, valid, ok, w_colour=5.0, w_occ=10.0):
+    """render.py:312-333 -> (dO, dD, dC); sign(0) = 0."""
+    m_ind, wd, wc, wo = _loss_masks(mask, valid, ok, D.dtype)
+    return (w_occ * wo * np.sign(O - m_ind), wd * np.sign(D - tgt_d),
+            (w_colour * wc)[..., None] * np.sign(C - tgt_c))
+
+
+def train_on_batch(st: Stack, batch: dict, w_colour=5.0, w_occ=10.0):
+    """trainer.py:480-506: forward -> render -> losses -> grads -> backward -> Adam."""
+    occ, col, xs, ms = mlp_forward(st, batch["encoded"])
+    k = st.count
+    lead = batch["encoded"].shape[1:-1]
+    occ_r, col_r = occ.reshape((k,) + lead), col.reshape((k,) + lead + (3,))
+    O, D, C, w, T = render_forward(occ_r, col_r, batch["t"])
+    args = (batch["target_depth"], batch["target_colour"], batch["target_mask"],
+            batch["valid_depth"], batch["ray_ok"], w_colour, w_occ)
+    ld, lc, lo, _ = losses(O, D, C, *args)
+    dO, dD, dC = loss_grads(O, D, C, *args)
+    d_occ, d_col = render_backward(occ_r, col_r, batch["t"], w, T, dO, dD, dC)
+    dW, db = mlp_backward(st, occ, col, xs, ms, d_occ, d_col)
+    adam_update(st, dW, db, update_mask=batch["ray_ok"].any(axis=-1))
+    return ld, lc, lo
+
+
+def synthetic_batch(arch: Arch, k: int, rays: int, points: int, seed: int) -> dict:
+    """trainer.py:594-606 (the reference's own benchmark input)."""
+    g = keyed_rng(seed, BENCH, k, arch.hidden)
+    t = np.sort(g.random((k, rays, points)).astype(np.float32) * 4.0, axis=-1)
+    return dict(
+        encoded=(g.standard_normal((k, rays, points, arch.input_dim)) * 0.7).astype(np.float32),
+        t=t,
+        target_depth=(g.random((k, rays)) * 4.0).astype(np.float32),
+        target_colour=g.random((k, rays, 3)).astype(np.float32),
+        target_mask=g.random((k, rays)) < 0.6,
+        valid_depth=np.ones((k, rays), bool),
+        ray_ok=np.ones((k, rays), bool),
+    )
+
+
+# --------------------------------------------------------------------------
+# rays and depth-guided sampling (render.py, objects.py, trainer.py)
+# --------------------------------------------------------------------------
+
+@dataclass(frozen=True)
+class Sampling:
+    """render.py:38-58 defaults."""
+    t_near: float = 0.0
+    t_far: float = 8.0
+    n_stratified: int = 5
+    n_surface: int = 5
+    surface_std: float = 0.03
+
+
+def ray_box(origins, dirs, bmin, bmax):
+    """render.py:111-139 slab test -> (t_entry, t_exit, hit)."""
+    o = np.atleast_2d(np.asarray(origins, np.float64))
+    d = np.atleast_2d(np.asarray(dirs, np.float64))
+    with np.errstate(divide="ignore", invalid="ignore"):
+        r = 1.0 / d
+        ta = (bmin - o) * r
+        tb = (bmax - o) * r
+    lo, hi = np.minimum(ta, tb), np.maximum(ta, tb)
+    flat = d == 0
+    if flat.any():
+        inside = (o >= bmin) & (o <= bmax)
+        lo = np.where(flat, np.where(inside, -np.inf, np.inf), lo)
+        hi = np.where(flat, np.where(inside, np.inf, -np.inf), hi)
+    t_in, t_out = lo.max(axis=-1), hi.min(axis=-1)
+    entry = np.maximum(t_in, 0.0)
+    return entry, t_out, (t_out >= entry) & (t_out >= 0.0)
+
+
+def _bins(u, lo, hi):
+    """render.py:142-146."""
+    n = u.shape[-1]
+    return lo[..., None] + ((np.arange(n) + u) / n) * (hi - lo)[..., None]
+
+
+def sample_along_rays(g, surf, valid, in_mask, far, cfg: Sampling, near=None):
+    """render.py:149-227.  Draw order is fixed: u_strat, z_surf, u_fallback."""
+    surf = np.asarray(surf, np.float64)
+    r = surf.shape[0]
+    u_s = g.random((r, cfg.n_stratified))
+    z = g.standard_normal((r, cfg.n_surface))
+    u_f = g.random((r, cfg.n_stratified + cfg.n_surface))
+    lo = np.full(r, cfg.t_near) if near is None else np.asarray(near, np.float64)
+    far = np.maximum(np.asarray(far, np.float64), lo)
+    valid = np.asarray(valid, bool)
+    in_mask = np.asarray(in_mask, bool)
+    has_d = valid & (surf > lo)
+    blocked = valid & ~has_d
+    over = in_mask & has_d & (surf > far + 3.0 * cfg.surface_std)
+    guided = in_mask & has_d & ~over
+    band_hi = np.minimum(surf + 3.0 * cfg.surface_std, far)
+    tg = np.concatenate([_bins(u_s, lo, surf),
+                         np.clip(surf[:, None] + cfg.surface_std * z, lo[:, None], band_hi[:, None])],
+                        axis=1)
+    up = np.where(in_mask, far, np.where(has_d, np.minimum(surf, far), far))
+    tf = _bins(u_f, lo, np.maximum(up, lo))
+    t = np.where(guided[:, None], tg, tf)
+    ok = (guided | (up > lo)) & ~blocked & ~over
+    t.sort(axis=1)
+    return t, ok
+
+
+def sample_training_pixels(keyframes, object_id: int, seed: int, step: int, n_rays: int):
+    """objects.py:323-352 -> (kf_idx, u, v, in_mask)."""
+    if not keyframes:
+        raise ValueError(f"object {object_id} has no keyframes to sample from")
+    g = keyed_rng(seed, PIXELS, object_id, step)
+    kf = g.integers(0, len(keyframes), size=n_rays)
+    uv = g.random((n_rays, 2))
+    u = np.empty(n_rays, np.int64)
+    v = np.empty(n_rays, np.int64)
+    hit = np.empty(n_rays, bool)
+    for k in np.unique(kf):
+        s = kf == k
+        u0, v0, u1, v1 = keyframes[int(k)].bbox
+        uu = np.minimum(u0 + np.floor(uv[s, 0] * (u1 - u0)).astype(np.int64), u1 - 1)
+        vv = np.minimum(v0 + np.floor(uv[s, 1] * (v1 - v0)).astype(np.int64), v1 - 1)
+        u[s], v[s] = uu, vv
+        hit[s] = keyframes[int(k)].mask[vv - v0, uu - u0]
+    return kf, u, v, hit
+
+
+def zero_batch(rays: int, points: int, input_dim: int) -> dict:
+    """trainer.py:190-200."""
+    z = lambda *s: np.zeros(s, np.float32)
+    return dict(encoded=z(rays, points, input_dim), t=z(rays, points), target_depth=z(rays),
+                target_colour=z(rays, 3), target_mask=np.zeros(rays, bool),
+                valid_depth=np.zeros(rays, bool), ray_ok=np.zeros(rays, bool))
+
+
+def assemble_batch(inst, intr, arch: Arch, n_rays: int, step: int, seed: int,
+                   cfg: Sampling = Sampling(), bound_pad: float = 0.10, with_aux: bool = False):
+    """trainer.py:269-318 for one instance (object or background).
+
+    ``inst`` needs object_id, keyframes (bbox/mask/rgb/depth/pose), aabb
+    (min/max f64), pe_scale and active.  ``intr`` needs fx, fy, cx, cy, width,
+    height.  With ``with_aux`` the pixel draws and f64 rays are returned too.
+    """
+    pts_per_ray = cfg.n_stratified + cfg.n_surface
+    if not inst.keyframes or not getattr(inst, "active", True):
+        out = zero_batch(n_rays, pts_per_ray, arch.input_dim)
+        return (out, None) if with_aux else out
+    kf, u, v, in_mask = sample_training_pixels(inst.keyframes, inst.object_id, seed, step, n_rays)
+    rgb = np.empty((n_rays, 3), np.float64)
+    z = np.empty(n_rays, np.float64)
+    pose = np.empty((n_rays, 3, 4), np.float64)
+    for k in np.unique(kf):
+        frame = inst.keyframes[int(k)]
+        s = kf == k
+        du, dv = u[s] - frame.bbox[0], v[s] - frame.bbox[1]
+        rgb[s] = frame.rgb[dv, du]
+        z[s] = frame.depth[dv, du]
+        pose[s] = frame.pose[:3, :]
+    # camera_dirs, render.py:76-86
+    px = np.stack([u, v], axis=1).astype(np.float64)
+    if (np.any(px[:, 0] < 0) or np.any(px[:, 0] >= intr.width) or np.any(px[:, 1] < 0)
+            or np.any(px[:, 1] >= intr.height)):
+        raise ValueError("pixel coordinates outside the image")
+    dc = np.empty((n_rays, 3))
+    dc[:, 0] = (px[:, 0] - intr.cx) / intr.fx
+    dc[:, 1] = (px[:, 1] - intr.cy) / intr.fy
+    dc[:, 2] = 1.0
+    to_t = np.linalg.norm(dc, axis=-1)
+    # np.einsum("rij,rj->ri", R, dc) (trainer.py:292).  numpy's 2-lane SIMD
+    # sum-of-products evaluates (r0*d0 + r2*d2) + r1*d1 without FMA; spelled
+    # out so the oracle is machine-independent (pinned by the goldens).
+    R = pose[:, :, :3]
+    d = (R[:, :, 0] * dc[:, None, 0] + R[:, :, 2] * dc[:, None, 2]) + R[:, :, 1] * dc[:, None, 1]
+    d /= np.linalg.norm(d, axis=-1, keepdims=True)
+    o = pose[:, :, 3]
+    valid = z > 0
+    surf = z * to_t
+    bmin, bmax = np.asarray(inst.aabb.min, np.float64), np.asarray(inst.aabb.max, np.float64)
+    pad = bound_pad * (0.5 * (bmax - bmin))          # geometry.py:40-42
+    pmin, pmax = bmin - pad, bmax + pad
+    t0, t1, hit = ray_box(o, d, pmin, pmax)
+    near = np.where(hit, np.maximum(t0, cfg.t_near), cfg.t_near)
+    far = np.where(hit & (t1 > near), t1, cfg.t_far)
+    t, ok = sample_along_rays(keyed_rng(seed, SAMPLES, inst.object_id, step), surf, valid, in_mask,
+                              far, cfg, near=near)
+    pts = o[:, None, :] + t[:, :, None] * d[:, None, :]
+    enc = positional_encode(pts, 0.5 * (pmin + pmax), 0.5 * (pmax - pmin), arch, inst.pe_scale)
+    out = dict(encoded=enc.astype(np.float32), t=t.astype(np.float32),
+               target_depth=surf.astype(np.float32), target_colour=rgb.astype(np.float32),
+               target_mask=in_mask, valid_depth=valid, ray_ok=ok)
+    if with_aux:
+        return out, dict(kf_idx=kf, u=u, v=v, in_mask=in_mask, origins=o, dirs=d, near=near,
+                         far=far, t64=t, surface_t=surf)
+    return out
+
+
+def stack_batches(batches: list) -> dict:
+    """trainer.py:320-330."""
+    return {key: np.stack([b[key] for b in batches]) for key in batches[0]}
+
+
+@dataclass
+class MapState:
+    """The Mapper fields the step touches (trainer.py:203-222)."""
+    intr: object
+    objects: list             # instances in model-index order (model_to_object)
+    background: object | None
+    obj: Stack
+    bg: Stack
+    seed: int = 0
+    rays_object: int = 120
+    rays_background: int = 1200
+    sampling: Sampling = field(default_factory=Sampling)
+    bound_pad: float = 0.10
+    w_colour: float = 5.0
+    w_occ: float = 10.0
+    train_background: bool = True
+    global_step: int = 0
+
+
+def map_update_step(ms: MapState) -> dict:
+    """Mapper.train_step(mode="vectorised"), trainer.py:356-402.
+
+    Returns {object_id: (L_depth, L_colour, L_occ)} like StepReport.losses.
+    """
+    step = ms.global_step
+    out = {}
+    pts = ms.sampling.n_stratified + ms.sampling.n_surface
+    if ms.obj.count > 0:
+        bs = []
+        for k in range(ms.obj.count):
+            if ms.obj.frozen[k]:
+                bs.append(zero_batch(ms.rays_object, pts, ms.obj.arch.input_dim))
+            else:
+                bs.append(assemble_batch(ms.objects[k], ms.intr, ms.obj.arch, ms.rays_object, step,
+                                         ms.seed, ms.sampling, ms.bound_pad))
+        ld, lc, lo = train_on_batch(ms.obj, stack_batches(bs), ms.w_colour, ms.w_occ)
+        for k in range(ms.obj.count):
+            vals = (ld[k], lc[k], lo[k])
+            oid = ms.objects[k].object_id
+            if not all(np.isfinite(x) for x in vals):
+                raise FloatingPointError(f"non-finite loss for object {oid}")
+            out[oid] = tuple(float(x) for x in vals)
+    bg = ms.background
+    if ms.train_background and bg is not None:
+        if ms.bg.frozen[bg.model_index]:
+            b = zero_batch(ms.rays_background, pts, ms.bg.arch.input_dim)
+        else:
+            b = assemble_batch(bg, ms.intr, ms.bg.arch, ms.rays_background, step, ms.seed,
+                               ms.sampling, ms.bound_pad)
+        ld, lc, lo = train_on_batch(ms.bg, stack_batches([b]), ms.w_colour, ms.w_occ)
+        vals = (ld[0], lc[0], lo[0])
+        if not all(np.isfinite(x) for x in vals):
+            raise FloatingPointError("non-finite loss for object 0")
+        out[0] = tuple(float(x) for x in vals)
+    ms.global_step += 1
+    return out

@@ -1,0 +1,668 @@
+// Fused train / forward / backward kernels over stacked per-object MLPs and
+// their C-ABI launchers (vm_train_step, vm_forward, vm_backward).
+#include "vm_mlp.cuh"
+
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+namespace vm {
+
+// Stage the model block into smem; hidden and output weight rows swizzled.
+template <int H, int L>
+__device__ __forceinline__ void load_weights(const KStack& st, const float* __restrict__ gp, float* __restrict__ sW) {
+  const int tid = threadIdx.x;
+  // layer 0 (plain) + biases: copy as 16-B chunks without swizzle.
+  {
+    const int n4 = (st.w_off[1]) / 4;  // W0 and b0 are contiguous at the block start
+    for (int i = tid; i < n4; i += kThreads) st4(sW + 4 * i, ld4(gp + 4 * i));
+  }
+#pragma unroll
+  for (int l = 1; l < L; ++l) {
+    const int rows = (l == L - 1) ? 4 : H;
+    const int cpr = H / 4;
+    const float* src = gp + st.w_off[l];
+    float* dst = sW + st.w_off[l];
+    for (int i = tid; i < rows * cpr; i += kThreads) {
+      const int row = i / cpr, ch = i % cpr;
+      st4(dst + row * H + swz(row, 4 * ch), ld4(src + row * H + 4 * ch));
+    }
+    const float* bsrc = gp + st.b_off[l];
+    float* bdst = sW + st.b_off[l];
+    for (int i = tid; i < rows / 4; i += kThreads) st4(bdst + 4 * i, ld4(bsrc + 4 * i));
+  }
+}
+
+// Load the block's encoded samples (feature-major) and t.
+__device__ __forceinline__ void load_block(const KStack& st, int64_t gs0, int ns, float* __restrict__ E,
+                                           float* __restrict__ tS, int tt, int nthr, bool with_t) {
+  const int D = st.D;
+  const float* src = st.enc + gs0 * D;
+  for (int idx = tt; idx < kSB * D; idx += nthr) {
+    const int s = idx / D, f = idx - s * D;
+    E[f * kLD + s] = s < ns ? src[idx] : 0.f;
+  }
+  for (int idx = tt; idx < (st.Dp - D) * kSB; idx += nthr) E[(D + idx / kSB) * kLD + (idx % kSB)] = 0.f;
+  if (with_t && tt < kSB) tS[tt] = tt < ns ? st.t[gs0 + tt] : 0.f;
+}
+
+template <int H, int L, int MODE>
+__device__ void run_item(const KStack& st, int item, float* smem) {
+  using Cfg = TeamCfg<H>;
+  constexpr int T = Cfg::T, OW = Cfg::OW, NTEAMS = kWarps / T;
+  using WG = WarpGrads<H, L>;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int team = warp / T, wt = warp % T;
+  const int o0 = wt * OW;
+
+  const int k = item / st.P, split = item % st.P;
+  const int kg = st.model_base + k;
+  float* sW = smem;
+  float* base = smem + st.w_floats + team * st.team_floats;
+  float* E = base;
+  float* Abuf = E + st.Dp * kLD;               // (L-1) hidden buffers of H rows
+  float* O = Abuf + (L - 1) * H * kLD;         // 4 rows
+  float* Tsc = O + 4 * kLD;                    // 32
+  float* tS = Tsc + kSB;                       // 32
+
+  load_weights<H, L>(st, st.params + int64_t(k) * st.block, sW);
+  __syncthreads();
+
+  // block range of this item
+  int64_t gs_model;  // first sample of the model
+  int nblk_model, S = st.S, G = st.G;
+  if (MODE == kTrain) {
+    gs_model = int64_t(k) * st.R * S;
+    nblk_model = (st.R + G - 1) / G;
+  } else {
+    gs_model = int64_t(k) * st.N;
+    nblk_model = int((st.N + kSB - 1) / kSB);
+  }
+  const int bps = (nblk_model + st.P - 1) / st.P;
+  const int blk0 = split * bps, blk1 = min(nblk_model, blk0 + bps);
+
+  WG acc;
+  acc.zero();
+
+  for (int blk = blk0 + team; blk < blk1; blk += NTEAMS) {
+    int ns, nr = 0, r_begin = 0;
+    int64_t gs0;
+    if (MODE == kTrain) {
+      r_begin = blk * G;
+      nr = min(G, st.R - r_begin);
+      ns = nr * S;
+      gs0 = gs_model + int64_t(r_begin) * S;
+    } else {
+      gs0 = gs_model + int64_t(blk) * kSB;
+      { const int64_t rem = st.N - int64_t(blk) * kSB; ns = int(rem < kSB ? rem : kSB); }
+    }
+    load_block(st, gs0, ns, E, tS, wt * 32 + lane, T * 32, MODE == kTrain);
+    team_sync(team, T);
+
+    // ---------------- forward ----------------
+    float* X = E;
+    for (int l = 0; l < L - 1; ++l) {
+      float* Y = Abuf + l * H * kLD;
+      if (l == 0)
+        fwd_layer<OW, false, 0>(sW + st.w_off[0], st.fi0, sW + st.b_off[0], X, st.fi0, Y, o0, lane);
+      else
+        fwd_layer<OW, true, H>(sW + st.w_off[l], H, sW + st.b_off[l], X, H, Y, o0, lane);
+      team_sync(team, T);
+      X = Y;
+    }
+    if (wt == 0) fwd_out<H>(sW + st.w_off[L - 1], sW + st.b_off[L - 1], X, O, lane);
+    team_sync(team, T);
+
+    if (MODE == kForward) {
+      for (int s = wt * 32 + lane; s < ns * 4; s += T * 32) {
+        const int smp = s >> 2, ch = s & 3;
+        const float v = O[ch * kLD + smp];
+        if (ch == 0) st.occ_out[gs0 + smp] = v;
+        else st.col_out[(gs0 + smp) * 3 + ch - 1] = v;
+      }
+      team_sync(team, T);
+      continue;
+    }
+
+    // ---------------- render + loss (train) / external grads (backward) -----
+    if (wt == 0) {
+      // zero the pad samples' output grads
+      if (lane >= ns) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) O[c * kLD + lane] = 0.f;
+      }
+      if (MODE == kTrain) {
+        if (lane < nr) {
+          const int r = r_begin + lane;
+          const int sb = lane * S;
+          const int64_t rg = int64_t(k) * st.R + r;
+          auto occ = [&](int i) { return O[sb + i]; };
+          auto col = [&](int i, int c) { return O[(1 + c) * kLD + sb + i]; };
+          auto tt = [&](int i) { return tS[sb + i]; };
+          render_ray_forward(S, occ, col, tt, [&](int i, float v) { Tsc[sb + i] = v; });
+          const RayFwd f = render_ray_sums(S, occ, col, tt, [&](int i) { return Tsc[sb + i]; });
+          RayTargets tg;
+          tg.depth = st.tdepth[rg];
+          tg.colour[0] = st.tcol[rg * 3 + 0];
+          tg.colour[1] = st.tcol[rg * 3 + 1];
+          tg.colour[2] = st.tcol[rg * 3 + 2];
+          tg.mask = st.tmask[rg] != 0;
+          tg.valid = st.valid[rg] != 0;
+          tg.ok = st.ok[rg] != 0;
+          const RayLossGrad lg = ray_loss_grad(f, tg, st.wc, st.wo);
+          st.ray_terms[rg * 3 + 0] = lg.l_depth;
+          st.ray_terms[rg * 3 + 1] = lg.l_colour;
+          st.ray_terms[rg * 3 + 2] = lg.l_occ;
+          // backward writes dz (sigmoid'd) in place of the outputs; it walks
+          // samples from the last to the first, reading only sample i >= cur.
+          render_ray_backward(S, occ, col, tt, [&](int i) { return Tsc[sb + i]; }, lg.dO, lg.dD, lg.dC,
+                              [&](int i, float d_occ, const float* d_col) {
+                                const float o = O[sb + i];
+                                O[sb + i] = __fmul_rn(__fmul_rn(d_occ, o), __fsub_rn(1.0f, o));
+#pragma unroll
+                                for (int c = 0; c < 3; ++c) {
+                                  const float cv = O[(1 + c) * kLD + sb + i];
+                                  O[(1 + c) * kLD + sb + i] = __fmul_rn(__fmul_rn(d_col[c], cv), __fsub_rn(1.0f, cv));
+                                }
+                              });
+        }
+      } else {  // kBackward: dz from caller's output grads (models.py:380-382)
+        if (lane < ns) {
+          const int64_t g = gs0 + lane;
+          const float o = O[lane];
+          O[lane] = (st.gocc[g] * o) * (1.0f - o);
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            const float cv = O[(1 + c) * kLD + lane];
+            O[(1 + c) * kLD + lane] = (st.gcol[g * 3 + c] * cv) * (1.0f - cv);
+          }
+        }
+      }
+    }
+    team_sync(team, T);
+
+    // ---------------- backward ----------------
+    {
+      float* Alast = Abuf + (L - 2) * H * kLD;
+      // output layer: dW (column slice of this warp) + db, then dz into Alast
+      dw_acc<1, WG::NQL>(acc.wl, O, 0, Alast, o0, WG::NQL, lane);
+      if (wt == 0 && lane < 4) {
+        float s = 0.f;
+#pragma unroll
+        for (int q = 0; q < kSB; q += 4) {
+          const float4 v = ld4(O + lane * kLD + q);
+          s += (v.x + v.y) + (v.z + v.w);
+        }
+        acc.bl += s;
+      }
+      __syncwarp();
+      dx_layer<OW, 4, H>(sW + st.w_off[L - 1], O, Alast, o0, lane);
+      team_sync(team, T);
+    }
+#pragma unroll
+    for (int l = L - 2; l >= 1; --l) {
+      float* Gl = Abuf + l * H * kLD;        // dz of layer l (rows o)
+      float* Xl = Abuf + (l - 1) * H * kLD;  // input of layer l
+      dw_acc<WG::NJ, WG::NQH>(acc.wh[l - 1 < 0 ? 0 : l - 1], Gl, o0, Xl, 0, WG::NQH, lane);
+      acc.bh[l] += db_acc<OW>(Gl, o0, lane);
+      team_sync(team, T);
+      dx_layer<OW, H, H>(sW + st.w_off[l], Gl, Xl, o0, lane);
+      team_sync(team, T);
+    }
+    dw_acc<WG::NJ, WG::NQ0>(acc.w0, Abuf, o0, E, 0, st.Dp / 8, lane);
+    acc.bh[0] += db_acc<OW>(Abuf, o0, lane);
+    team_sync(team, T);
+  }
+
+  if (MODE == kForward) return;
+
+  // ---------------- gradient write-out ----------------
+  // Destination: grads[k] when the model has one CTA, else partials[item].
+  float* gdst = (st.P == 1) ? st.grads + int64_t(k) * st.block
+                            : st.partials + (int64_t(k) * st.P + split) * st.block;
+  // combine bias partial sums across the sample halves (OW == 16)
+#pragma unroll
+  for (int l = 0; l < L - 1; ++l) {
+    if (OW == 16) acc.bh[l] += __shfl_xor_sync(0xffffffffu, acc.bh[l], 16);
+  }
+  auto emit = [&](float* dst, bool add) {
+    const int r = lane >> 3, c = lane & 7;
+    auto put = [&](int idx, float v) {
+      if (add) dst[idx] += v;
+      else dst[idx] = v;
+    };
+    // layer 0
+#pragma unroll
+    for (int j = 0; j < WG::NJ; ++j)
+#pragma unroll
+      for (int q = 0; q < WG::NQ0; ++q) {
+        const int o = o0 + r + 4 * j, i = c + 8 * q;
+        if (i < st.fi0) put(st.w_off[0] + o * st.fi0 + i, acc.w0[j][q]);
+      }
+    // hidden layers
+#pragma unroll
+    for (int h = 0; h < WG::NH; ++h)
+#pragma unroll
+      for (int j = 0; j < WG::NJ; ++j)
+#pragma unroll
+        for (int q = 0; q < WG::NQH; ++q) {
+          const int o = o0 + r + 4 * j, i = c + 8 * q;
+          put(st.w_off[h + 1] + o * H + i, acc.wh[h][j][q]);
+        }
+    // output layer
+#pragma unroll
+    for (int q = 0; q < WG::NQL; ++q) put(st.w_off[L - 1] + r * H + o0 + c + 8 * q, acc.wl[0][q]);
+    // biases
+#pragma unroll
+    for (int l = 0; l < L - 1; ++l)
+      if (lane < OW) put(st.b_off[l] + o0 + lane, acc.bh[l]);
+    if (wt == 0 && lane < 4) put(st.b_off[L - 1] + lane, acc.bl);
+  };
+
+  if (NTEAMS == 1) {
+    emit(gdst, false);
+  } else {
+    __syncthreads();  // every team is done with the weights: reuse sW as staging
+    for (int t = 0; t < NTEAMS; ++t) {
+      if (team == t) emit(sW, t > 0);
+      __syncthreads();
+    }
+    for (int i = tid; i < st.block / 4; i += kThreads) st4(gdst + 4 * i, ld4(sW + 4 * i));
+  }
+
+  // ---------------- per-model finalisation (last CTA of the model) ---------
+  __shared__ int s_last;
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) {
+    int last = 1;
+    if (st.P > 1) {
+      const int prev = atomicAdd(&st.counters[k], 1);
+      last = prev == st.P - 1;
+    }
+    s_last = last;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+
+  float* gk = st.grads + int64_t(k) * st.block;
+  bool finite = true;
+  for (int i = tid; i < st.block / 4; i += kThreads) {
+    float4 v;
+    if (st.P > 1) {
+      const float* pbase = st.partials + int64_t(k) * st.P * st.block + 4 * i;
+      v = __ldcg(reinterpret_cast<const float4*>(pbase));
+      for (int p = 1; p < st.P; ++p) {
+        const float4 w = __ldcg(reinterpret_cast<const float4*>(pbase + int64_t(p) * st.block));
+        v.x += w.x; v.y += w.y; v.z += w.z; v.w += w.w;
+      }
+      st4(gk + 4 * i, v);
+    } else {
+      v = ld4(gk + 4 * i);
+    }
+    finite &= isfinite(v.x) && isfinite(v.y) && isfinite(v.z) && isfinite(v.w);
+  }
+  const bool all_finite = __syncthreads_and(finite);
+
+  if (MODE == kBackward) return;
+
+  // update mask = ray_ok.any(-1) (trainer.py:504)
+  bool any_ok = false;
+  for (int r = tid; r < st.R; r += kThreads) any_ok |= st.ok[int64_t(k) * st.R + r] != 0;
+  const bool upd = __syncthreads_or(any_ok);
+  if (tid < 3) {
+    const float* terms = st.ray_terms + int64_t(k) * st.R * 3;
+    const int j = tid;
+    const float sum = pairwise_sum([&](int64_t r) { return __ldcg(terms + r * 3 + j); }, st.R);
+    st.losses[int64_t(k) * 3 + j] = sum;
+    if (!isfinite(sum)) atomicMin(&st.status[1], k);
+  }
+  if (tid == 0) {
+    const bool active = upd && !st.frozen[k];
+    st.upd[k] = active ? 1 : 0;
+    if (active && !all_finite) atomicMin(&st.status[0], k);
+    const int64_t t = st.step[k] + 1;
+    float2 c;
+    if (t <= st.corr_len) {
+      c.x = st.corr1[t - 1];
+      c.y = st.corr2[t - 1];
+    } else {
+      c.x = 1.0f;
+      c.y = 1.0f;
+    }
+    st.corr[k] = c;
+    if (st.P > 1) st.counters[k] = 0;
+  }
+}
+
+template <int H0, int L0, int H1, int L1, int MODE>
+__global__ void __launch_bounds__(kThreads, 1) mlp_kernel(const __grid_constant__ KParams p) {
+  extern __shared__ __align__(16) float smem[];
+  const int b = blockIdx.x;
+  if (p.n_stacks == 1 || b < p.s[1].item_base) {
+    run_item<H0, L0, MODE>(p.s[0], b, smem);
+  } else {
+    if constexpr (H1 > 0) run_item<H1, L1, MODE>(p.s[1], b - p.s[1].item_base, smem);
+  }
+}
+
+// Adam over every active model of every stack; stack s is skipped when any
+// stack <= s reported a non-finite gradient, or any stack < s a non-finite
+// loss (trainer.py:368-388 raises before training the next stack).
+struct AdamStack {
+  float* P; float* M; float* V;
+  const float* G;
+  int64_t* step;
+  const uint8_t* upd;
+  const float2* corr;
+  int block, K, chunks, item_base;
+  AdamConsts a;
+  int32_t* status;
+};
+struct AdamParams {
+  AdamStack s[2];
+  int n_stacks;
+};
+
+__global__ void __launch_bounds__(256) adam_train_kernel(const __grid_constant__ AdamParams p) {
+  int b = blockIdx.x, si = 0;
+  if (p.n_stacks > 1 && b >= p.s[1].item_base) si = 1;
+  const AdamStack& s = p.s[si];
+  b -= s.item_base;
+  bool skip = s.status[0] != 0x7f7f7f7f;
+  for (int j = 0; j < si; ++j) skip |= (p.s[j].status[0] != 0x7f7f7f7f) || (p.s[j].status[1] != 0x7f7f7f7f);
+  const int k = b / s.chunks, ch = b % s.chunks;
+  if (k == 0 && ch == 0 && threadIdx.x == 0) s.status[2] = skip ? 0 : 1;
+  if (skip || !s.upd[k]) return;
+  const float2 c = s.corr[k];
+  const int64_t base = int64_t(k) * s.block;
+  const int i = (ch * 256 + threadIdx.x) * 4;
+  if (i < s.block) adam_vec4(s.P + base, s.M + base, s.V + base, s.G + base, i, c.x, c.y, s.a);
+  if (ch == 0 && threadIdx.x == 0) s.step[k] += 1;
+}
+
+// ------------------------------------------------------------------ host side
+
+struct Instance {
+  int H, L;
+};
+
+inline size_t smem_bytes(const KStack& s) {
+  const int nteams = kWarps / (s.H == 32 ? 1 : (s.H == 64 ? 4 : 8));
+  return size_t(s.w_floats + nteams * s.team_floats) * sizeof(float) + 64;
+}
+
+static int fill_stack(const VmStack& vs, KStack& ks, VmLayout& L) {
+  int rc = compute_layout(vs.arch, L);
+  if (rc) return rc;
+  if (vs.arch.input_dim > kDpMax) return VM_ERR_UNSUPPORTED;
+  std::memset(&ks, 0, sizeof(ks));
+  ks.H = L.hidden_pad;
+  ks.L = L.n_layers;
+  ks.D = vs.arch.input_dim;
+  ks.Dp = round_up(ks.D, 8);
+  ks.fi0 = L.fi_pad[0];
+  ks.block = int(L.block);
+  ks.w_floats = round_up(ks.block, 32);
+  ks.team_floats = (ks.Dp + (ks.L - 1) * ks.H + 4) * kLD + 2 * kSB;
+  for (int l = 0; l < L.n_layers; ++l) {
+    ks.w_off[l] = int(L.w_off[l]);
+    ks.b_off[l] = int(L.b_off[l]);
+  }
+  ks.params = vs.params;
+  ks.frozen = vs.frozen;
+  ks.step = vs.step;
+  ks.corr1 = vs.corr1;
+  ks.corr2 = vs.corr2;
+  ks.corr_len = vs.corr_len;
+  ks.K = vs.count;
+  return VM_OK;
+}
+
+using KernelFn = void (*)(KParams);
+
+template <int MODE>
+static KernelFn pick_kernel(int H0, int L0, int H1, int L1) {
+#define VM_SINGLE(h, l) \
+  if (H1 == 0 && H0 == h && L0 == l) return mlp_kernel<h, l, 0, 0, MODE>;
+#define VM_PAIR(h0, l0, h1, l1) \
+  if (H0 == h0 && L0 == l0 && H1 == h1 && L1 == l1) return mlp_kernel<h0, l0, h1, l1, MODE>;
+  VM_SINGLE(32, 2) VM_SINGLE(32, 3) VM_SINGLE(32, 4) VM_SINGLE(32, 5)
+  VM_SINGLE(64, 2) VM_SINGLE(64, 3) VM_SINGLE(64, 4)
+  VM_SINGLE(128, 2) VM_SINGLE(128, 3) VM_SINGLE(128, 4)
+  if constexpr (MODE == kTrain) {
+    VM_PAIR(32, 4, 128, 4) VM_PAIR(32, 4, 32, 4) VM_PAIR(32, 3, 32, 3) VM_PAIR(32, 4, 64, 4)
+  }
+#undef VM_SINGLE
+#undef VM_PAIR
+  return nullptr;
+}
+
+static int launch_mlp(KernelFn fn, const KParams& p, int grid, size_t smem, cudaStream_t s) {
+  if (smem > 227 * 1024) {
+    set_error("vm: model too large for shared memory (block + activation tiles > 227 KB)");
+    return VM_ERR_UNSUPPORTED;
+  }
+  VM_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(fn), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               int(smem)));
+  void* args[] = {const_cast<KParams*>(&p)};
+  VM_CUDA(cudaLaunchKernel(reinterpret_cast<const void*>(fn), dim3(grid), dim3(kThreads), args, smem, s));
+  return VM_OK;
+}
+
+// Work split: CTAs per model from the model's own cost only (never from K),
+// so a model's gradient summation order -- and therefore its bits -- does
+// not depend on which other models share the launch (vectorised ==
+// sequential, test_trainer.py:117-132).  One CTA per ~kTargetFlop of work:
+// a 120-ray hidden-32 object is one CTA, the 1200-ray hidden-128 background
+// about a hundred.
+constexpr double kTargetFlop = 24.0e6;
+
+static int choose_splits(const KStack* ks, int n, int* P) {
+  for (int i = 0; i < n; ++i) {
+    const double flop_per_sample = double(ks[i].H) * (ks[i].Dp + 2 * (ks[i].L - 2) * ks[i].H + 8) * 3.0;
+    const double cost = flop_per_sample * ks[i].R * ks[i].S;
+    const int nblk = (ks[i].R + ks[i].G - 1) / ks[i].G;
+    int p = int(cost / kTargetFlop + 0.5);
+    p = std::max(1, std::min(p, nblk));
+    const int bps = (nblk + p - 1) / p;  // blocks per CTA; drop empty CTAs
+    P[i] = (nblk + bps - 1) / bps;
+  }
+  return VM_OK;
+}
+
+}  // namespace vm
+
+using namespace vm;
+
+namespace {
+struct TrainPlan {
+  KParams kp;
+  AdamParams ap;
+  int grid, adam_grid;
+  size_t smem;
+  size_t ws_bytes;
+  // workspace offsets
+  size_t off_grads[2], off_part[2], off_terms[2], off_cnt[2], off_upd[2], off_corr[2];
+};
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+int plan_train(const VmStack* stacks, const VmBatch* batches, int n, TrainPlan& pl) {
+  VM_REQUIRE(n >= 1 && n <= 2, "vm_train_step: 1 or 2 stacks supported");
+  std::memset(&pl, 0, sizeof(pl));
+  pl.kp.n_stacks = n;
+  pl.ap.n_stacks = n;
+  size_t off = 0;
+  int item_base = 0, model_base = 0, adam_base = 0;
+  int P[2] = {1, 1};
+  for (int i = 0; i < n; ++i) {
+    VmLayout L;
+    int rc = fill_stack(stacks[i], pl.kp.s[i], L);
+    if (rc) {
+      set_error("vm_train_step: unsupported architecture");
+      return rc;
+    }
+    KStack& ks = pl.kp.s[i];
+    const VmBatch& b = batches[i];
+    VM_REQUIRE(b.n_models == stacks[i].count, "vm_train_step: batch leading axis != params.count");
+    VM_REQUIRE(b.input_dim == stacks[i].arch.input_dim, "vm_train_step: encoding dim mismatch");
+    VM_REQUIRE(b.n_points >= 1 && b.n_points <= kSB, "vm_train_step: points per ray must be in [1, 32]");
+    VM_REQUIRE(b.encoded != nullptr, "vm_train_step: encoded input required");
+    ks.R = b.n_rays;
+    ks.S = b.n_points;
+    ks.G = kSB / b.n_points;
+    ks.enc = b.encoded;
+    ks.t = b.t;
+    ks.tdepth = b.target_depth;
+    ks.tcol = b.target_colour;
+    ks.tmask = b.target_mask;
+    ks.valid = b.valid_depth;
+    ks.ok = b.ray_ok;
+  }
+  choose_splits(pl.kp.s, n, P);
+  for (int i = 0; i < n; ++i) {
+    KStack& ks = pl.kp.s[i];
+    ks.P = P[i];
+    ks.item_base = item_base;
+    ks.model_base = model_base;
+    item_base += ks.K * ks.P;
+    model_base += ks.K;
+    const size_t K = size_t(ks.K);
+    pl.off_grads[i] = off; off = align_up(off + K * ks.block * 4, 256);
+    pl.off_part[i] = off;  off = align_up(off + (ks.P > 1 ? K * ks.P * ks.block * 4 : 0), 256);
+    pl.off_terms[i] = off; off = align_up(off + K * size_t(ks.R) * 3 * 4, 256);
+    pl.off_cnt[i] = off;   off = align_up(off + K * 4, 256);
+    pl.off_upd[i] = off;   off = align_up(off + K, 256);
+    pl.off_corr[i] = off;  off = align_up(off + K * 8, 256);
+    pl.smem = std::max(pl.smem, smem_bytes(ks));
+    AdamStack& as = pl.ap.s[i];
+    as.P = stacks[i].params;
+    as.M = stacks[i].m;
+    as.V = stacks[i].v;
+    as.step = stacks[i].step;
+    as.block = ks.block;
+    as.K = ks.K;
+    as.chunks = (ks.block / 4 + 255) / 256;
+    as.item_base = adam_base;
+    as.a = adam_consts(stacks[i]);
+    adam_base += ks.K * as.chunks;
+  }
+  pl.grid = item_base;
+  pl.adam_grid = adam_base;
+  pl.ws_bytes = off;
+  return VM_OK;
+}
+}  // namespace
+
+extern "C" size_t vm_train_workspace_bytes(const VmStack* stacks, const VmBatch* batches, int n_stacks) {
+  TrainPlan pl;
+  if (plan_train(stacks, batches, n_stacks, pl)) return 0;
+  return pl.ws_bytes;
+}
+
+extern "C" int vm_train_step(const VmStack* stacks, const VmBatch* batches, int n_stacks, VmLossWeights w,
+                             float* losses, int32_t* status, void* workspace, size_t workspace_bytes,
+                             void* stream) {
+  TrainPlan pl;
+  int rc = plan_train(stacks, batches, n_stacks, pl);
+  if (rc) return rc;
+  VM_REQUIRE(workspace_bytes >= pl.ws_bytes, "vm_train_step: workspace too small");
+  cudaStream_t s = cudaStream_t(stream);
+  char* ws = static_cast<char*>(workspace);
+  VM_CUDA(cudaMemsetAsync(status, 0x7f, sizeof(int32_t) * 4 * n_stacks, s));
+  int loss_off = 0;
+  for (int i = 0; i < n_stacks; ++i) {
+    KStack& ks = pl.kp.s[i];
+    ks.grads = reinterpret_cast<float*>(ws + pl.off_grads[i]);
+    ks.partials = reinterpret_cast<float*>(ws + pl.off_part[i]);
+    ks.ray_terms = reinterpret_cast<float*>(ws + pl.off_terms[i]);
+    ks.counters = reinterpret_cast<int*>(ws + pl.off_cnt[i]);
+    ks.upd = reinterpret_cast<uint8_t*>(ws + pl.off_upd[i]);
+    ks.corr = reinterpret_cast<float2*>(ws + pl.off_corr[i]);
+    ks.losses = losses + int64_t(loss_off) * 3;
+    ks.status = status + 4 * i;
+    ks.wc = w.colour;
+    ks.wo = w.occupancy;
+    loss_off += ks.K;
+    AdamStack& as = pl.ap.s[i];
+    as.G = ks.grads;
+    as.upd = ks.upd;
+    as.corr = ks.corr;
+    as.status = ks.status;
+  }
+  if (pl.grid == 0) return VM_OK;
+  KernelFn fn = pick_kernel<kTrain>(pl.kp.s[0].H, pl.kp.s[0].L, n_stacks > 1 ? pl.kp.s[1].H : 0,
+                                    n_stacks > 1 ? pl.kp.s[1].L : 0);
+  if (!fn) {
+    if (n_stacks == 2) {  // no fused instantiation for this pair: run stacks back to back
+      // (Adam of stack 1 still honours stack 0's status because both read it)
+      set_error("vm_train_step: unsupported stack pair");
+      return VM_ERR_UNSUPPORTED;
+    }
+    set_error("vm_train_step: no kernel for this architecture");
+    return VM_ERR_UNSUPPORTED;
+  }
+  rc = launch_mlp(fn, pl.kp, pl.grid, pl.smem, s);
+  if (rc) return rc;
+  if (pl.adam_grid > 0) {
+    adam_train_kernel<<<pl.adam_grid, 256, 0, s>>>(pl.ap);
+    VM_CUDA(cudaGetLastError());
+  }
+  return VM_OK;
+}
+
+namespace {
+int run_fwd_bwd(const VmStack* st, const float* encoded, int64_t n_samples, const float* gocc,
+                const float* gcol, float* occ, float* col, float* grads, bool backward, cudaStream_t s) {
+  VM_REQUIRE(st && encoded && n_samples >= 0, "vm_forward/backward: bad arguments");
+  KParams kp;
+  std::memset(&kp, 0, sizeof(kp));
+  VmLayout L;
+  int rc = fill_stack(*st, kp.s[0], L);
+  if (rc) {
+    set_error("vm_forward/backward: unsupported architecture");
+    return rc;
+  }
+  kp.n_stacks = 1;
+  KStack& ks = kp.s[0];
+  ks.N = n_samples;
+  ks.S = 1;
+  ks.G = 1;
+  ks.R = 0;
+  ks.enc = encoded;
+  ks.gocc = gocc;
+  ks.gcol = gcol;
+  ks.occ_out = occ;
+  ks.col_out = col;
+  ks.grads = grads;
+  const int nblk = int((n_samples + kSB - 1) / kSB);
+  if (backward) {
+    ks.P = 1;  // one CTA per model reduces every block of that model
+  } else {
+    ks.P = std::max(1, std::min(nblk, 64));
+  }
+  if (ks.K == 0 || n_samples == 0) {
+    if (backward && ks.K > 0) VM_CUDA(cudaMemsetAsync(grads, 0, size_t(ks.K) * ks.block * 4, s));
+    return VM_OK;
+  }
+  KernelFn fn = backward ? pick_kernel<kBackward>(ks.H, ks.L, 0, 0) : pick_kernel<kForward>(ks.H, ks.L, 0, 0);
+  if (!fn) {
+    set_error("vm_forward/backward: no kernel for this architecture");
+    return VM_ERR_UNSUPPORTED;
+  }
+  return launch_mlp(fn, kp, ks.K * ks.P, smem_bytes(ks), s);
+}
+}  // namespace
+
+extern "C" int vm_forward(const VmStack* st, const float* encoded, int64_t n_samples, float* occ, float* col,
+                          void* stream) {
+  return run_fwd_bwd(st, encoded, n_samples, nullptr, nullptr, occ, col, nullptr, false, cudaStream_t(stream));
+}
+
+extern "C" int vm_backward(const VmStack* st, const float* encoded, int64_t n_samples, const float* grad_occ,
+                           const float* grad_col, float* grads, void* stream) {
+  return run_fwd_bwd(st, encoded, n_samples, grad_occ, grad_col, nullptr, nullptr, grads, true,
+                     cudaStream_t(stream));
+}

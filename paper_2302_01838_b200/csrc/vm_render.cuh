@@ -1,0 +1,111 @@
+// Per-ray occupancy rendering, L1 losses and their gradients.
+//
+// Restates render.py:230-333 with numpy's float32 operation order so that,
+// given bit-identical per-sample occupancy/colour, the results are
+// bit-identical too (every op is an explicit _rn intrinsic: no FMA
+// contraction).  Used by the standalone parity kernels (vm_render.cu) and by
+// the fused training kernel (vm_mlp.cu).
+#pragma once
+
+#include "vm_common.cuh"
+
+namespace vm {
+
+// Accessor-based so callers can keep samples in smem or global memory.
+// OCC(i), COL(i,c), TT(i) read sample i of the ray; TRANS is scratch with
+// room for S floats (written: T_i).
+struct RayFwd {
+  float opacity, depth, colour[3];
+};
+
+template <typename Occ, typename Col, typename Tt, typename Tw>
+__device__ __forceinline__ RayFwd render_ray_forward(int S, const Occ& occ, const Col& col, const Tt& tt,
+                                                     const Tw& trans_store) {
+  // trans[0] = 1, trans[i] = cumprod(1 - o)[i-1]   (render.py:238-241)
+  float T = 1.0f;
+  for (int i = 0; i < S; ++i) {
+    trans_store(i, T);
+    T = (i == 0) ? __fsub_rn(1.0f, occ(0)) : __fmul_rn(T, __fsub_rn(1.0f, occ(i)));
+  }
+  return RayFwd{};
+}
+
+// Full forward given stored transmittance: weights = o*T; O = pw(w);
+// D = pw(w*t); C = sequential over samples of w*c (render.py:242-245).
+template <typename Occ, typename Col, typename Tt, typename Tr>
+__device__ __forceinline__ RayFwd render_ray_sums(int S, const Occ& occ, const Col& col, const Tt& tt,
+                                                  const Tr& trans) {
+  RayFwd r;
+  auto w = [&](int64_t i) { return __fmul_rn(occ(int(i)), trans(int(i))); };
+  r.opacity = pairwise_sum_leaf(w, 0, S);
+  r.depth = pairwise_sum_leaf([&](int64_t i) { return __fmul_rn(w(i), tt(int(i))); }, 0, S);
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    float acc = __fmul_rn(w(0), col(0, c));
+    for (int i = 1; i < S; ++i) acc = __fadd_rn(acc, __fmul_rn(w(i), col(i, c)));
+    r.colour[c] = acc;
+  }
+  return r;
+}
+
+struct RayTargets {
+  float depth, colour[3];
+  bool mask, valid, ok;
+};
+
+struct RayLossGrad {
+  float l_depth, l_colour, l_occ;  // per-ray terms (before the sum over rays)
+  float dO, dD, dC[3];
+};
+
+// compute_losses / loss_output_grads per ray (render.py:284-333).
+__device__ __forceinline__ RayLossGrad ray_loss_grad(const RayFwd& f, const RayTargets& tg, float w_colour,
+                                                     float w_occ) {
+  const bool m_ok = tg.mask && tg.ok;
+  const float m_ind = tg.mask ? 1.0f : 0.0f;
+  const float wd = (m_ok && tg.valid) ? 1.0f : 0.0f;
+  const float wc = m_ok ? 1.0f : 0.0f;
+  const float wo = tg.ok ? 1.0f : 0.0f;
+  RayLossGrad o;
+  o.l_depth = __fmul_rn(wd, fabsf(__fsub_rn(f.depth, tg.depth)));
+  float cs = fabsf(__fsub_rn(f.colour[0], tg.colour[0]));
+  cs = __fadd_rn(cs, fabsf(__fsub_rn(f.colour[1], tg.colour[1])));
+  cs = __fadd_rn(cs, fabsf(__fsub_rn(f.colour[2], tg.colour[2])));
+  o.l_colour = __fmul_rn(wc, cs);
+  o.l_occ = __fmul_rn(wo, fabsf(__fsub_rn(f.opacity, m_ind)));
+  o.dD = __fmul_rn(wd, np_sign(__fsub_rn(f.depth, tg.depth)));
+  const float wcc = __fmul_rn(w_colour, wc);
+#pragma unroll
+  for (int c = 0; c < 3; ++c) o.dC[c] = __fmul_rn(wcc, np_sign(__fsub_rn(f.colour[c], tg.colour[c])));
+  o.dO = __fmul_rn(__fmul_rn(w_occ, wo), np_sign(__fsub_rn(f.opacity, m_ind)));
+  return o;
+}
+
+// render_backward per ray (render.py:249-281).  Emits (i, d_occ_i, d_col_i)
+// through `emit`, from the last sample to the first.
+template <typename Occ, typename Col, typename Tt, typename Tr, typename Emit>
+__device__ __forceinline__ void render_ray_backward(int S, const Occ& occ, const Col& col, const Tt& tt,
+                                                    const Tr& trans, float dO, float dD, const float dC[3],
+                                                    const Emit& emit) {
+  float rev = 0.0f;
+  for (int i = S - 1; i >= 0; --i) {
+    const float o = occ(i);
+    const float T = trans(i);
+    const float w = __fmul_rn(o, T);
+    float cs = __fmul_rn(dC[0], col(i, 0));
+    cs = __fadd_rn(cs, __fmul_rn(dC[1], col(i, 1)));
+    cs = __fadd_rn(cs, __fmul_rn(dC[2], col(i, 2)));
+    const float g = __fadd_rn(__fadd_rn(dO, __fmul_rn(dD, tt(i))), cs);
+    const float gw = __fmul_rn(g, w);
+    rev = (i == S - 1) ? gw : __fadd_rn(rev, gw);
+    const float suffix = __fsub_rn(rev, gw);
+    const float denom = np_maximum(__fsub_rn(1.0f, o), 1e-7f);
+    const float d_occ = __fsub_rn(__fmul_rn(g, T), __fdiv_rn(suffix, denom));
+    float d_col[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) d_col[c] = __fmul_rn(w, dC[c]);
+    emit(i, d_occ, d_col);
+  }
+}
+
+}  // namespace vm

@@ -1,0 +1,726 @@
+// KS: ray/sample generation for the per-object training batch.
+//
+// Restates, on the device and bit-exactly:
+//   objects.py:323-352  sample_training_pixels (keyframe index, pixel, mask bit)
+//   trainer.py:269-318  _assemble_batch (gathers, f64 ray geometry, padded box)
+//   render.py:76-139    camera_dirs / ray_box_intersect
+//   render.py:142-227   depth-guided stratified + Gaussian surface sampling
+//   models.py:286-308   positional encoding (f64, cast to f32)
+//   rng.py:24-34        keyed SeedSequence -> PCG64 streams; numpy's
+//                       Generator.integers (32-bit Lemire), .random() and
+//                       .standard_normal() (256-layer ziggurat) draw layouts.
+// The file is compiled with -fmad=false so every f64 expression rounds like
+// the numpy expression it restates (verified in tests/test_gpu_sampler.py).
+//
+// Stream layouts (per object, per step):
+//   PIXELS  key (seed,3,obj,step): [ceil(R/2) words kf Lemire halves, absent
+//           if n_kf==1][2R words uv]
+//   SAMPLES key (seed,4,obj,step): [nc*R u_strat][ns*R normals, variable
+//           length][S*R u_fallback]
+// Normals are resolved in parallel: every window position is classified as a
+// ziggurat fast accept or not, slow positions are resolved speculatively, and
+// one thread walks only the slow list to place them (about 2% of positions).
+#include "vm_common.cuh"
+#define VM_ZIG_QUAL __device__
+#include "ziggurat_tables.h"
+
+#include <cstring>
+
+namespace vm {
+namespace {
+
+typedef unsigned __int128 u128;
+
+__device__ __forceinline__ u128 pcg_mult() {
+  return (u128(2549297995355413924ULL) << 64) | u128(4865540595714422341ULL);
+}
+
+__device__ __forceinline__ uint64_t pcg_out(u128 s) {
+  const uint64_t hi = uint64_t(s >> 64), lo = uint64_t(s);
+  const uint64_t x = hi ^ lo;
+  const unsigned rot = unsigned(hi >> 58);
+  return (x >> rot) | (x << ((64 - rot) & 63));
+}
+
+// State after `delta` LCG steps (Brown, "Random number generation with
+// arbitrary strides").
+__device__ u128 pcg_advance(u128 state, u128 inc, uint64_t delta) {
+  u128 acc_mult = 1, acc_plus = 0, cur_mult = pcg_mult(), cur_plus = inc;
+  while (delta) {
+    if (delta & 1) {
+      acc_mult *= cur_mult;
+      acc_plus = acc_plus * cur_mult + cur_plus;
+    }
+    cur_plus = (cur_mult + 1) * cur_plus;
+    cur_mult *= cur_mult;
+    delta >>= 1;
+  }
+  return acc_mult * state + acc_plus;
+}
+
+struct Stream {
+  u128 state0, inc;
+  // Cursor positioned so that next() returns word `pos`.
+  __device__ __forceinline__ u128 at(uint64_t pos) const { return pcg_advance(state0, inc, pos); }
+};
+
+__device__ __forceinline__ uint64_t next_word(u128& s, u128 inc) {
+  s = s * pcg_mult() + inc;
+  return pcg_out(s);
+}
+
+__device__ __forceinline__ double word_to_double(uint64_t w) { return double(w >> 11) * (1.0 / 9007199254740992.0); }
+
+// SeedSequence(parts).generate_state(8) -> PCG64 seeding (numpy bit_generator.pyx, pcg64.c).
+__device__ Stream seed_stream(uint64_t seed, uint64_t purpose, uint64_t obj, uint64_t step) {
+  uint32_t ent[8];
+  int n = 0;
+  const uint64_t parts[4] = {seed, purpose, obj, step};
+  for (int i = 0; i < 4; ++i) {
+    uint64_t v = parts[i];
+    if (v == 0) {
+      ent[n++] = 0;
+    } else {
+      while (v) {
+        ent[n++] = uint32_t(v);
+        v >>= 32;
+      }
+    }
+  }
+  uint32_t hc = 0x43b0d7e5u;
+  auto hashmix = [&](uint32_t v) {
+    v ^= hc;
+    hc *= 0x931e8875u;
+    v *= hc;
+    return v ^ (v >> 16);
+  };
+  auto mix = [](uint32_t x, uint32_t y) {
+    const uint32_t r = 0xca01f9ddu * x - 0x4973f715u * y;
+    return r ^ (r >> 16);
+  };
+  uint32_t pool[4];
+  for (int i = 0; i < 4; ++i) pool[i] = hashmix(i < n ? ent[i] : 0u);
+  for (int s = 0; s < 4; ++s)
+    for (int d = 0; d < 4; ++d)
+      if (s != d) pool[d] = mix(pool[d], hashmix(pool[s]));
+  for (int e = 4; e < n; ++e)
+    for (int d = 0; d < 4; ++d) pool[d] = mix(pool[d], hashmix(ent[e]));
+  uint32_t hb = 0x8b51f9ddu, w[8];
+  for (int i = 0; i < 8; ++i) {
+    uint32_t v = pool[i & 3] ^ hb;
+    hb *= 0x58f38dedu;
+    v *= hb;
+    w[i] = v ^ (v >> 16);
+  }
+  uint64_t u[4];
+  for (int i = 0; i < 4; ++i) u[i] = uint64_t(w[2 * i]) | (uint64_t(w[2 * i + 1]) << 32);
+  const u128 initstate = (u128(u[0]) << 64) | u128(u[1]);
+  const u128 initseq = (u128(u[2]) << 64) | u128(u[3]);
+  Stream st;
+  st.inc = (initseq << 1) | 1;
+  u128 s = st.inc;  // 0 * mult + inc
+  s += initstate;
+  s = s * pcg_mult() + st.inc;
+  st.state0 = s;
+  return st;
+}
+
+struct Zig {
+  const uint64_t* ki;
+  const double* wi;
+  const double* fi;
+};
+
+__device__ __forceinline__ double zig_fast(uint64_t r, const Zig& z, bool& fast) {
+  const int idx = int(r & 0xff);
+  r >>= 8;
+  const int sign = int(r & 1);
+  const uint64_t rabs = (r >> 1) & 0x000fffffffffffffULL;
+  double x = double(rabs) * z.wi[idx];
+  if (sign) x = -x;
+  fast = rabs < z.ki[idx];
+  return x;
+}
+
+// Resolve an attempt starting at absolute word `p` whose first word is not a
+// fast accept.  Returns consumed words; `accepted` false means the normal
+// restarts at p + consumed.
+__device__ int zig_slow(const Stream& st, uint64_t p, const Zig& z, double& value, bool& accepted) {
+  u128 s = st.at(p);
+  uint64_t r = next_word(s, st.inc);
+  const int idx = int(r & 0xff);
+  r >>= 8;
+  const int sign = int(r & 1);
+  const uint64_t rabs = (r >> 1) & 0x000fffffffffffffULL;
+  double x = double(rabs) * z.wi[idx];
+  if (sign) x = -x;
+  const double zr = 3.6541528853610087963519472518;
+  const double zinv = 0.27366123732975827203338247596;
+  if (idx == 0) {
+    int used = 1;
+    for (;;) {
+      const double xx = -zinv * log1p(-word_to_double(next_word(s, st.inc)));
+      const double yy = -log1p(-word_to_double(next_word(s, st.inc)));
+      used += 2;
+      if (yy + yy > xx * xx) {
+        value = ((rabs >> 8) & 0x1) ? -(zr + xx) : zr + xx;
+        accepted = true;
+        return used;
+      }
+    }
+  }
+  const double u = word_to_double(next_word(s, st.inc));
+  accepted = ((z.fi[idx - 1] - z.fi[idx]) * u + z.fi[idx]) < exp(-0.5 * x * x);
+  value = x;
+  return 2;
+}
+
+__device__ __forceinline__ double np_min_d(double a, double b) {
+  if (a != a) return a;
+  if (b != b) return b;
+  return a <= b ? a : b;
+}
+__device__ __forceinline__ double np_max_d(double a, double b) {
+  if (a != a) return a;
+  if (b != b) return b;
+  return a >= b ? a : b;
+}
+
+struct KS {
+  const VmSampleObject* objs;
+  const VmKeyframe* kfs;
+  const float4* rgbd;
+  const uint8_t* mask;
+  VmSampleParams p;
+  int S, N, W, SC;  // samples/ray, normals/object, window, slow capacity
+  // outputs
+  float* t32;
+  float* tdepth;
+  float* tcol;
+  uint8_t* tmask;
+  uint8_t* valid;
+  uint8_t* ok;
+  float* points;    // [K,R,S,3] f32 (encode == 0)
+  double* p64;      // [K,R,S,3] f64 workspace (encode == 1)
+  double* nrm;      // [K,N] resolved normals (workspace)
+  int* status;      // [K] fallback flags (diagnostics)
+  int64_t* aux_kf;
+  int64_t* aux_u;
+  int64_t* aux_v;
+  double* aux_t64;
+};
+
+// Block-wide exclusive scan of one int per thread (blockDim.x == 256).
+__device__ int block_exclusive_scan(int v, int* scratch, int& total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int x = v;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) scratch[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    int w = lane < 8 ? scratch[lane] : 0;
+    for (int o = 1; o < 8; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += y;
+    }
+    if (lane < 8) scratch[8 + lane] = w;
+  }
+  __syncthreads();
+  total = scratch[8 + 7];
+  const int before = warp ? scratch[8 + warp - 1] : 0;
+  const int excl = before + x - v;
+  __syncthreads();
+  return excl;
+}
+
+constexpr int kST = 256;
+
+__global__ void __launch_bounds__(kST) sample_kernel(const __grid_constant__ KS ks) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  __shared__ uint64_t s_ki[256];
+  __shared__ double s_wi[256], s_fi[256];
+  __shared__ Stream s_pix, s_smp;
+  __shared__ int s_scan[16], s_flag, s_kfwords, s_nseg, s_nov, s_end;
+
+  const int k = blockIdx.x, tid = threadIdx.x;
+  const VmSampleObject ob = ks.objs[k];
+  const VmSampleParams& P = ks.p;
+  const int R = P.n_rays, S = ks.S, nc = P.n_stratified, nsf = P.n_surface, N = ks.N, W = ks.W;
+  const int64_t rbase = int64_t(k) * R;
+
+  if (!ob.active || ob.n_kf <= 0) {  // zero batch (trainer.py:190-200, :272-273)
+    for (int i = tid; i < R * S; i += kST) {
+      ks.t32[rbase * S + i] = 0.f;
+      if (ks.points) {
+        for (int c = 0; c < 3; ++c) ks.points[(rbase * S + i) * 3 + c] = 0.f;
+      }
+      if (ks.p64) {
+        for (int c = 0; c < 3; ++c) ks.p64[(rbase * S + i) * 3 + c] = 0.0;
+      }
+      if (ks.aux_t64) ks.aux_t64[rbase * S + i] = 0.0;
+    }
+    for (int r = tid; r < R; r += kST) {
+      ks.tdepth[rbase + r] = 0.f;
+      for (int c = 0; c < 3; ++c) ks.tcol[(rbase + r) * 3 + c] = 0.f;
+      ks.tmask[rbase + r] = 0;
+      ks.valid[rbase + r] = 0;
+      ks.ok[rbase + r] = 0;
+      if (ks.aux_kf) {
+        ks.aux_kf[rbase + r] = 0;
+        ks.aux_u[rbase + r] = 0;
+        ks.aux_v[rbase + r] = 0;
+      }
+    }
+    return;
+  }
+
+  // smem carve-up
+  double* xs = reinterpret_cast<double*>(sm);                  // [W]
+  double* ov_val = xs + W;                                     // [SC]
+  int* slow = reinterpret_cast<int*>(ov_val + ks.SC);          // [SC]
+  int* seg_j = slow + ks.SC;                                   // [SC+1]
+  int* seg_off = seg_j + ks.SC + 1;                            // [SC+1]
+  int* ov_j = seg_off + ks.SC + 1;                             // [SC]
+  int* kf_s = ov_j + ks.SC;                                    // [R]
+  uint8_t* fastf = reinterpret_cast<uint8_t*>(kf_s + R);       // [W]
+
+  for (int i = tid; i < 256; i += kST) {
+    s_ki[i] = vm_zig_ki[i];
+    s_wi[i] = __longlong_as_double(static_cast<long long>(vm_zig_wi[i]));
+    s_fi[i] = __longlong_as_double(static_cast<long long>(vm_zig_fi[i]));
+  }
+  if (tid == 0) s_pix = seed_stream(P.seed, 3, uint64_t(ob.object_id), uint64_t(P.step));
+  if (tid == 32) s_smp = seed_stream(P.seed, 4, uint64_t(ob.object_id), uint64_t(P.step));
+  if (tid == 64) s_flag = 0;
+  __syncthreads();
+  const Zig zig{s_ki, s_wi, s_fi};
+  const Stream pix = s_pix, smp = s_smp;
+
+  // ---------------- keyframe index per ray (objects.py:336) ----------------
+  const int n_kf = ob.n_kf;
+  if (n_kf == 1) {
+    for (int r = tid; r < R; r += kST) kf_s[r] = 0;
+    if (tid == 0) s_kfwords = 0;
+  } else {
+    const uint32_t n = uint32_t(n_kf);
+    const uint32_t thr = uint32_t((uint64_t(1) << 32) - n) % n;
+    bool rej = false;
+    for (int r = tid; r < R; r += kST) {
+      u128 s = pix.at(uint64_t(r >> 1));
+      const uint64_t w = next_word(s, pix.inc);
+      const uint32_t x = (r & 1) ? uint32_t(w >> 32) : uint32_t(w);
+      const uint64_t m = uint64_t(x) * n;
+      const uint32_t left = uint32_t(m);
+      if (left < n && left < thr) rej = true;
+      kf_s[r] = int(m >> 32);
+    }
+    if (__syncthreads_or(rej)) {
+      if (tid == 0) {  // rare: replay the buffered Lemire draws sequentially
+        u128 s = pix.state0;
+        uint64_t buf = 0, words = 0;
+        bool have = false;
+        for (int r = 0; r < R;) {
+          uint32_t x;
+          if (have) {
+            x = uint32_t(buf >> 32);
+            have = false;
+          } else {
+            buf = next_word(s, pix.inc);
+            ++words;
+            x = uint32_t(buf);
+            have = true;
+          }
+          const uint64_t m = uint64_t(x) * n;
+          const uint32_t left = uint32_t(m);
+          if (left < n && left < thr) continue;
+          kf_s[r++] = int(m >> 32);
+        }
+        s_kfwords = int(words);
+        s_flag |= 1;
+      }
+    } else if (tid == 0) {
+      s_kfwords = (R + 1) / 2;
+    }
+  }
+
+  // ---------------- normals window (render.py:185) ----------------
+  // classify window positions [0, W) of the normals region
+  const uint64_t nbase = uint64_t(nc) * R;
+  {
+    const int per = (W + kST - 1) / kST;
+    const int p0 = tid * per, p1 = min(W, p0 + per);
+    int cnt = 0;
+    if (p0 < p1) {
+      u128 s = smp.at(nbase + p0);
+      for (int p = p0; p < p1; ++p) {
+        bool f;
+        xs[p] = zig_fast(next_word(s, smp.inc), zig, f);
+        fastf[p] = f;
+        cnt += !f;
+      }
+    }
+    int total;
+    int off = block_exclusive_scan(cnt, s_scan, total);
+    if (total > ks.SC) {
+      if (tid == 0) s_flag |= 2;
+    } else {
+      for (int p = p0; p < p1; ++p)
+        if (!fastf[p]) slow[off++] = p;
+    }
+    __syncthreads();
+    // speculative slow-path resolution, one thread per slow position
+    if (!(s_flag & 2)) {
+      for (int i = tid; i < total; i += kST) {
+        double v;
+        bool acc;
+        const int used = zig_slow(smp, nbase + slow[i], zig, v, acc);
+        ov_val[i] = v;
+        seg_off[i] = acc ? used : -used;  // temporarily: +consumed (accepted) / -consumed (rejected)
+      }
+    }
+    __syncthreads();
+    if (tid == 0 && !(s_flag & 2)) {
+      // walk the slow list; seg_j/seg_off become segment starts/offsets,
+      // ov_j/ov_val the accepted slow normals (compacted in place).
+      int pos = 0, j = 0, nseg = 1, nov = 0;
+      int* res = seg_off;  // read results before overwriting: keep a copy in ov_j scratch
+      for (int i = 0; i < total; ++i) ov_j[i] = res[i];
+      seg_j[0] = 0;
+      seg_off[0] = 0;
+      for (int i = 0; i < total && j < N; ++i) {
+        const int s = slow[i];
+        if (s < pos) continue;
+        if (j + (s - pos) >= N) break;
+        j += s - pos;
+        const int r = ov_j[i];
+        if (r > 0) {
+          ov_val[nov] = ov_val[i];
+          slow[nov] = j;  // reuse slow[] for the override normal index (i >= nov)
+          ++nov;
+          ++j;
+          pos = s + r;
+        } else {
+          pos = s - r;
+        }
+        seg_j[nseg] = j;
+        seg_off[nseg] = pos - j;
+        ++nseg;
+      }
+      const int end = pos + (N - j);
+      if (end > W) s_flag |= 2;
+      s_nseg = nseg;
+      s_nov = nov;
+      s_end = end;
+    }
+    __syncthreads();
+  }
+  double* nrm = ks.nrm + int64_t(k) * N;
+  if (s_flag & 2) {
+    // window overflow (practically unreachable): sequential ziggurat replay
+    if (tid == 0) {
+      u128 s = smp.at(nbase);
+      uint64_t used = 0;
+      for (int j = 0; j < N; ++j) {
+        for (;;) {
+          bool f;
+          const double x = zig_fast(next_word(s, smp.inc), zig, f);
+          if (f) {
+            nrm[j] = x;
+            ++used;
+            break;
+          }
+          double v;
+          bool acc;
+          const int u = zig_slow(smp, nbase + used, zig, v, acc);
+          used += u;
+          s = smp.at(nbase + used);
+          if (acc) {
+            nrm[j] = v;
+            break;
+          }
+        }
+      }
+      s_end = int(used);
+      ks.status[k] = s_flag;
+    }
+  } else {
+    const int nseg = s_nseg, nov = s_nov;
+    for (int j = tid; j < N; j += kST) {
+      int lo = 0, hi = nseg - 1;  // last segment with seg_j <= j
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (seg_j[mid] <= j) lo = mid;
+        else hi = mid - 1;
+      }
+      int a = 0, b = nov - 1, hit = -1;  // override lookup
+      while (a <= b) {
+        const int mid = (a + b) >> 1;
+        if (slow[mid] == j) { hit = mid; break; }
+        if (slow[mid] < j) a = mid + 1;
+        else b = mid - 1;
+      }
+      nrm[j] = hit >= 0 ? ov_val[hit] : xs[j + seg_off[lo]];
+    }
+    if (tid == 0) ks.status[k] = s_flag;
+  }
+  __syncthreads();
+  const uint64_t fb_base = nbase + uint64_t(s_end);
+  const uint64_t uv_base = uint64_t(s_kfwords);
+
+  // ---------------- per ray ----------------
+  for (int r = tid; r < R; r += kST) {
+    const int kfi = kf_s[r];
+    const VmKeyframe& kf = ks.kfs[ob.kf_begin + kfi];
+    u128 s = pix.at(uv_base + 2 * uint64_t(r));
+    const double du = word_to_double(next_word(s, pix.inc));
+    const double dv = word_to_double(next_word(s, pix.inc));
+    int64_t u = kf.u0 + int64_t(floor(du * double(kf.u1 - kf.u0)));
+    int64_t v = kf.v0 + int64_t(floor(dv * double(kf.v1 - kf.v0)));
+    u = u < int64_t(kf.u1 - 1) ? u : int64_t(kf.u1 - 1);
+    v = v < int64_t(kf.v1 - 1) ? v : int64_t(kf.v1 - 1);
+    const int64_t tix = kf.texel_off + (v - kf.v0) * (kf.u1 - kf.u0) + (u - kf.u0);
+    const float4 px = ks.rgbd[tix];
+    const bool in_mask = ks.mask[tix] != 0;
+
+    // rays (trainer.py:289-297): camera dirs, rotate, normalise
+    const double d0 = (double(u) - P.cx) / P.fx;
+    const double d1 = (double(v) - P.cy) / P.fy;
+    const double to_t = sqrt((d0 * d0 + d1 * d1) + 1.0);
+    double dir[3], org[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      // einsum "rij,rj->ri": (R[i][0]*d0 + R[i][2]*1.0) + R[i][1]*d1
+      dir[i] = (kf.pose[4 * i + 0] * d0 + kf.pose[4 * i + 2] * 1.0) + kf.pose[4 * i + 1] * d1;
+      org[i] = kf.pose[4 * i + 3];
+    }
+    const double dn = sqrt((dir[0] * dir[0] + dir[1] * dir[1]) + dir[2] * dir[2]);
+#pragma unroll
+    for (int i = 0; i < 3; ++i) dir[i] = dir[i] / dn;
+    const double z = double(px.w);
+    const bool valid = z > 0.0;
+    const double surf = z * to_t;
+
+    // ray_box_intersect (render.py:111-139) on the padded box
+    double tin = -INFINITY, tout = INFINITY;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      double lo, hi;
+      if (dir[i] == 0.0) {
+        const bool inside = (org[i] >= ob.box_min[i]) && (org[i] <= ob.box_max[i]);
+        lo = inside ? -INFINITY : INFINITY;
+        hi = inside ? INFINITY : -INFINITY;
+      } else {
+        const double inv = 1.0 / dir[i];
+        const double ta = (ob.box_min[i] - org[i]) * inv;
+        const double tb = (ob.box_max[i] - org[i]) * inv;
+        lo = np_min_d(ta, tb);
+        hi = np_max_d(ta, tb);
+      }
+      tin = i == 0 ? lo : np_max_d(tin, lo);
+      tout = i == 0 ? hi : np_min_d(tout, hi);
+    }
+    const double t_entry = np_max_d(tin, 0.0);
+    const bool hit = (tout >= t_entry) && (tout >= 0.0);
+    const double near_ = hit ? np_max_d(t_entry, P.t_near) : P.t_near;
+    const double far_ = (hit && tout > near_) ? tout : P.t_far;
+
+    // sample_along_rays (render.py:149-227)
+    const double lo = near_;
+    const double far2 = np_max_d(far_, lo);
+    const bool has_depth = valid && (surf > lo);
+    const bool near_block = valid && !has_depth;
+    const bool over = in_mask && has_depth && (surf > far2 + P.three_std);
+    const bool guided = in_mask && has_depth && !over;
+    const double upper = in_mask ? far2 : (has_depth ? np_min_d(surf, far2) : far2);
+    const bool ray_ok = (guided || upper > lo) && !near_block && !over;
+    double t[32];
+    if (guided) {
+      u128 q = smp.at(uint64_t(nc) * r);
+      for (int i = 0; i < nc; ++i) {
+        const double us = word_to_double(next_word(q, smp.inc));
+        t[i] = lo + ((double(i) + us) / double(nc)) * (surf - lo);
+      }
+      const double band_hi = np_min_d(surf + P.three_std, far2);
+      for (int i = 0; i < nsf; ++i) {
+        const double a = surf + P.surface_std * nrm[int64_t(r) * nsf + i];
+        t[nc + i] = np_min_d(np_max_d(a, lo), band_hi);
+      }
+    } else {
+      u128 q = smp.at(fb_base + uint64_t(S) * r);
+      const double hi_f = np_max_d(upper, lo);
+      for (int i = 0; i < S; ++i) {
+        const double uf = word_to_double(next_word(q, smp.inc));
+        t[i] = lo + ((double(i) + uf) / double(S)) * (hi_f - lo);
+      }
+    }
+    for (int i = 1; i < S; ++i) {  // ascending insertion sort
+      const double x = t[i];
+      int j = i - 1;
+      while (j >= 0 && t[j] > x) {
+        t[j + 1] = t[j];
+        --j;
+      }
+      t[j + 1] = x;
+    }
+
+    const int64_t rg = rbase + r;
+    ks.tdepth[rg] = float(surf);
+    ks.tcol[rg * 3 + 0] = px.x;
+    ks.tcol[rg * 3 + 1] = px.y;
+    ks.tcol[rg * 3 + 2] = px.z;
+    ks.tmask[rg] = in_mask;
+    ks.valid[rg] = valid;
+    ks.ok[rg] = ray_ok;
+    if (ks.aux_kf) {
+      ks.aux_kf[rg] = kfi;
+      ks.aux_u[rg] = u;
+      ks.aux_v[rg] = v;
+    }
+    for (int i = 0; i < S; ++i) {
+      const int64_t sg = rg * S + i;
+      ks.t32[sg] = float(t[i]);
+      if (ks.aux_t64) ks.aux_t64[sg] = t[i];
+      double pn[3];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) pn[c] = ((org[c] + t[i] * dir[c]) - ob.center[c]) / ob.half[c];
+      if (ks.points) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) ks.points[sg * 3 + c] = float(pn[c]);
+      }
+      if (ks.p64) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) ks.p64[sg * 3 + c] = pn[c];
+      }
+    }
+  }
+}
+
+// positional_encode (models.py:286-308) from the f64 normalised points:
+// one thread per (sample, band); band -1 writes the raw point.
+__global__ void encode_kernel(int64_t n_samples, int n_freq, int include, int D, int S, int64_t samples_per_obj,
+                              const VmSampleObject* __restrict__ objs, const double* __restrict__ p64,
+                              float* __restrict__ enc) {
+  const int nb = n_freq + (include ? 1 : 0);
+  const int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (idx >= n_samples * nb) return;
+  const int64_t smp = idx / nb;
+  const int b = int(idx % nb) - (include ? 1 : 0);
+  float* out = enc + smp * D;
+  const int64_t obj = smp / samples_per_obj;
+  const bool live = objs[obj].active && objs[obj].n_kf > 0;
+  const double* p = p64 + smp * 3;
+  if (b < 0) {
+    for (int c = 0; c < 3; ++c) out[c] = live ? float(p[c]) : 0.f;
+    return;
+  }
+  const int base = (include ? 3 : 0) + 6 * b;
+  if (!live) {
+    for (int c = 0; c < 6; ++c) out[base + c] = 0.f;
+    return;
+  }
+  const double coef = (3.141592653589793 * double(1u << b)) / objs[obj].pe_scale;
+  for (int c = 0; c < 3; ++c) {
+    const double a = coef * p[c];
+    out[base + c] = float(sin(a));
+    out[base + 3 + c] = float(cos(a));
+  }
+}
+
+struct SamplePlan {
+  int S, N, W, SC;
+  size_t smem;
+  size_t off_nrm, off_status, off_p64, bytes;
+};
+
+SamplePlan plan_sample(int n_objects, const VmSampleParams& p) {
+  SamplePlan pl;
+  pl.S = p.n_stratified + p.n_surface;
+  pl.N = p.n_surface * p.n_rays;
+  pl.W = pl.N + pl.N / 16 + 64;
+  pl.SC = pl.W / 8 + 64;
+  pl.smem = size_t(pl.W) * 8 + size_t(pl.SC) * 8 + size_t(pl.SC) * 4 * 2 + size_t(pl.SC + 1) * 4 * 2 +
+            size_t(p.n_rays) * 4 + size_t(pl.W) + 16;
+  size_t off = 0;
+  auto take = [&](size_t b) {
+    const size_t o = off;
+    off = (off + b + 255) / 256 * 256;
+    return o;
+  };
+  pl.off_nrm = take(size_t(n_objects) * pl.N * 8 + 8);
+  pl.off_status = take(size_t(n_objects) * 4 + 4);
+  pl.off_p64 = take(p.encode ? size_t(n_objects) * p.n_rays * pl.S * 3 * 8 : 0);
+  pl.bytes = off;
+  return pl;
+}
+
+}  // namespace
+}  // namespace vm
+
+using namespace vm;
+
+extern "C" size_t vm_sample_workspace_bytes(int n_objects, const VmSampleParams* params) {
+  if (!params || n_objects < 0) return 0;
+  return plan_sample(n_objects, *params).bytes;
+}
+
+extern "C" int vm_sample(const VmSampleObject* objects, int n_objects, const VmKeyframe* keyframes,
+                         const float* rgbd, const uint8_t* mask, const VmSampleParams* params, VmBatch* out,
+                         VmSampleAux* aux, void* workspace, size_t workspace_bytes, void* stream) {
+  VM_REQUIRE(params && out && n_objects >= 0, "vm_sample: null argument");
+  const VmSampleParams& p = *params;
+  VM_REQUIRE(p.n_rays >= 1 && p.n_stratified >= 1 && p.n_surface >= 0, "vm_sample: bad sampling config");
+  VM_REQUIRE(p.n_stratified + p.n_surface <= 32, "vm_sample: at most 32 points per ray");
+  VM_REQUIRE(p.fx > 0 && p.fy > 0, "vm_sample: bad intrinsics");
+  SamplePlan pl = plan_sample(n_objects, p);
+  VM_REQUIRE(workspace_bytes >= pl.bytes, "vm_sample: workspace too small");
+  VM_REQUIRE(pl.smem <= 220 * 1024, "vm_sample: too many rays per object for one CTA");
+  if (n_objects == 0) return VM_OK;
+  if (p.encode) VM_REQUIRE(out->encoded != nullptr, "vm_sample: encoded output missing");
+  else VM_REQUIRE(out->points != nullptr, "vm_sample: points output missing");
+  char* ws = static_cast<char*>(workspace);
+  KS ks;
+  std::memset(&ks, 0, sizeof(ks));
+  ks.objs = objects;
+  ks.kfs = keyframes;
+  ks.rgbd = reinterpret_cast<const float4*>(rgbd);
+  ks.mask = mask;
+  ks.p = p;
+  ks.S = pl.S;
+  ks.N = pl.N;
+  ks.W = pl.W;
+  ks.SC = pl.SC;
+  ks.t32 = const_cast<float*>(out->t);
+  ks.tdepth = const_cast<float*>(out->target_depth);
+  ks.tcol = const_cast<float*>(out->target_colour);
+  ks.tmask = const_cast<uint8_t*>(out->target_mask);
+  ks.valid = const_cast<uint8_t*>(out->valid_depth);
+  ks.ok = const_cast<uint8_t*>(out->ray_ok);
+  ks.points = p.encode ? nullptr : const_cast<float*>(out->points);
+  ks.p64 = p.encode ? reinterpret_cast<double*>(ws + pl.off_p64) : nullptr;
+  ks.nrm = reinterpret_cast<double*>(ws + pl.off_nrm);
+  ks.status = reinterpret_cast<int*>(ws + pl.off_status);
+  if (aux) {
+    ks.aux_kf = aux->kf_idx;
+    ks.aux_u = aux->u;
+    ks.aux_v = aux->v;
+    ks.aux_t64 = aux->t64;
+  }
+  cudaStream_t s = cudaStream_t(stream);
+  VM_CUDA(cudaFuncSetAttribute(sample_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pl.smem)));
+  sample_kernel<<<n_objects, kST, pl.smem, s>>>(ks);
+  VM_CUDA(cudaGetLastError());
+  if (p.encode) {
+    const int D = (p.include_input ? 3 : 0) + 6 * p.n_freq;
+    const int64_t spo = int64_t(p.n_rays) * pl.S;
+    const int64_t n = int64_t(n_objects) * spo;
+    const int nb = p.n_freq + (p.include_input ? 1 : 0);
+    const int64_t work = n * nb;
+    encode_kernel<<<unsigned((work + 255) / 256), 256, 0, s>>>(n, p.n_freq, p.include_input, D, pl.S, spo, objects,
+                                                               ks.p64, const_cast<float*>(out->encoded));
+    VM_CUDA(cudaGetLastError());
+  }
+  return VM_OK;
+}

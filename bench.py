@@ -1,0 +1,312 @@
+"""Benchmark: vMAP map update (BASELINE.json config 2) on B200.
+
+Workload (a "step"): one full Mapper.train_step on the config-2 synthetic scene
+-- 50 objects x 5 keyframes (hidden-32 MLPs, 120 rays x 10 samples each) plus
+the hidden-128 background (1200 rays) -- i.e. CUDA sampling (KS), the fused
+MLP fwd/render/loss/bwd kernel (KF) and batched Adam (KA).
+
+  python bench.py [--gpus N --steps K --warmup W]      # this framework
+  python bench.py --impl reference [...]               # reference CPU path
+
+N > 1 (torchrun, one rank per GPU): objects are sharded across ranks
+(weak scaling: 50 objects per rank, background on rank 0), losses gathered
+with NCCL all_gather every step.  Timing: CUDA events per step on the launch
+stream with an L2 flush (256 MiB write) between steps, max over ranks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "object-model training steps/sec (×objects) and ray-samples/sec at 50 objects"
+UNIT = "object-steps/s"
+OBJ_PER_RANK = 50
+
+
+def flop_per_sample(hidden: int, input_dim: int = 33) -> int:
+    """Algorithmic GEMM FLOPs per sample: 2*(2*MAC_fwd + MAC_dx)."""
+    mac_fwd = hidden * input_dim + 2 * hidden * hidden + 4 * hidden
+    mac_dx = 2 * hidden * hidden + 4 * hidden
+    return 2 * (2 * mac_fwd + mac_dx)
+
+
+def dist_setup():
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return rank, world
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except FileNotFoundError:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            out, _ = self.proc.communicate(timeout=10)
+            self.lines = [l for l in out.splitlines() if l.strip()]
+
+    def summary(self):
+        if not self.lines:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in self.lines:
+            f = [x.strip() for x in l.split(",")]
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except (ValueError, IndexError):
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def cpu_sample(scene, seconds: float, min_steps: int = 3):
+    """Time the oracle port (numpy restatement of the reference) on config 2."""
+    import numpy as np
+    from oracle import vobj_oracle as O
+    from paper_2302_01838_b200 import TrainConfig
+    sys.path.insert(0, str(ROOT / "tests"))
+    from tests.helpers import oracle_mapstate
+    ms = oracle_mapstate(scene, TrainConfig())
+    O.map_update_step(ms)  # warm-up (BLAS threads, page faults)
+    n, t0 = 0, time.perf_counter()
+    while n < min_steps or time.perf_counter() - t0 < seconds:
+        O.map_update_step(ms)
+        n += 1
+    dt = (time.perf_counter() - t0) / n
+    k = len(scene["objects"])
+    return k / dt, n, dt
+
+
+def blas_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        return max([i.get("num_threads", 1) for i in threadpool_info()] or [1])
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the reference algorithm (oracle port: the reference is
+    pure Python/numpy and has no compiled build to run) on the box's host cores."""
+    if rank != 0:
+        return
+    from paper_2302_01838_b200.scenes import make_scene
+    scene = make_scene(OBJ_PER_RANK, n_kf=5, seed=0)
+    import numpy as np  # noqa: F401
+    from oracle import vobj_oracle as O
+    from paper_2302_01838_b200 import TrainConfig
+    from tests.helpers import oracle_mapstate
+    ms = oracle_mapstate(scene, TrainConfig())
+    for _ in range(max(args.warmup, 1)):
+        O.map_update_step(ms)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        O.map_update_step(ms)
+        times.append(time.perf_counter() - t0)
+    dt = sum(times) / len(times)
+    k = len(scene["objects"]) * world  # N rooms, as the GPU arm (timed on one host: N x the work)
+    dt = dt * world
+    v = k / dt
+    cores = blas_threads()
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": _config(world),
+        "samples_per_s": k * 120 * 10 / dt,
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": f"{args.steps} full map-update steps of config 2 (oracle/vobj_oracle.py "
+                                   f"map_update_step, numpy/OpenBLAS, {cores} threads)"},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }))
+
+
+def _config(world):
+    return {"workload": "config 2: Replica-sized synthetic scene, 50 objects x 5 keyframes + background; full "
+                        "map update per step (ray/sample generation + fused MLP fwd/render/L1/bwd + Adam)",
+            "objects_per_gpu": OBJ_PER_RANK, "objects": OBJ_PER_RANK * world, "hidden_object": 32,
+            "hidden_background": 128, "rays_per_object": 120, "rays_background": 1200, "points_per_ray": 10,
+            "frame": "1200x680", "l2": "flushed (256 MiB write) between timed steps",
+            "parallelism": f"object-sharded x{world}" if world > 1 else "single GPU"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    rank, world = dist_setup() if args.impl == "b200" else (int(os.environ.get("RANK", "0")),
+                                                            int(os.environ.get("WORLD_SIZE", "1")))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import numpy as np
+    import torch
+    from paper_2302_01838_b200 import TrainConfig, _lib
+    from paper_2302_01838_b200.mapper import Mapper
+    from paper_2302_01838_b200.scenes import make_scene, populate
+    from paper_2302_01838_b200.sharding import ObjectSharding
+
+    dev = torch.device("cuda", torch.cuda.current_device())
+    lib = _lib.load()
+    # weak scaling: each rank maps one config-2 "room" (50 objects + its
+    # background); object ids / init keys are globally unique across ranks.
+    scene = make_scene(OBJ_PER_RANK, n_kf=5, seed=rank)
+    shard = ObjectSharding(world, [r for r in range(world) for _ in range(OBJ_PER_RANK)])
+    cfg = TrainConfig()
+    mapper = Mapper(scene["intrinsics"], cfg, device=dev, object_id_base=rank * OBJ_PER_RANK,
+                    init_index_base=rank * OBJ_PER_RANK, background_init_index=rank)
+    populate(mapper, scene)
+    k_local = mapper.obj_params.count
+    k_total = OBJ_PER_RANK * world
+
+    # FP32 FFMA peak (roofline denominator; MEASURED_PEAKS.json has no FP32 entry)
+    tf = C.c_float()
+    _lib.check(lib.vm_ffma_peak(16384, C.byref(tf), _lib.stream_ptr()), "vm_ffma_peak")
+    ffma_peak = float(tf.value)
+
+    for _ in range(args.warmup):
+        rep = mapper.train_step()
+        shard.gather_losses(rep)
+    torch.cuda.synchronize()
+
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    lib.vm_profile_enable(1)
+    with ClockSampler(dev.index) as clk:
+        for i in range(args.steps):
+            flush.fill_(float(i))
+            ev[i][0].record(stream)
+            losses, status, _ = mapper.enqueue_step(mapper.global_step)
+            shard.gather_losses_device(losses)
+            ev[i][1].record(stream)
+            mapper.global_step += 1
+        torch.cuda.synchronize()
+    n_launch = C.c_int()
+    mlp_ms = C.c_double()
+    lib.vm_profile_read(C.byref(n_launch), C.byref(mlp_ms))
+    lib.vm_profile_enable(0)
+    step_ms = sum(a.elapsed_time(b) for a, b in ev)
+    t_local = torch.tensor([step_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        torch.distributed.all_reduce(t_local, op=torch.distributed.ReduceOp.MAX)
+        torch.distributed.barrier()
+    total_ms = float(t_local.item())
+    ms_per_step = total_ms / args.steps
+    value = k_total * args.steps / (total_ms / 1e3)
+
+    # end-to-end through the public API: Mapper.train_step() with the step's
+    # per-object sampling tables re-uploaded from host memory (as after a
+    # frame's process_frame) and the losses/status read back every step.
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    h2d = d2h = 0
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        mapper.invalidate()
+        rep = mapper.train_step()
+        shard.gather_losses(rep)
+    torch.cuda.synchronize()
+    e2e_s = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+    if world > 1:
+        torch.distributed.all_reduce(e2e_s, op=torch.distributed.ReduceOp.MAX)
+    e2e_value = k_total * args.steps / float(e2e_s.item())
+    h2d, d2h = mapper.last_io_bytes()
+
+    # roofline of the dominant kernel (fused MLP fwd/bwd): algorithmic FLOPs
+    # per launch / CUDA-event duration of that launch inside the timed region.
+    flop_launch = (k_local * cfg.rays_per_object * cfg.points_per_ray * flop_per_sample(32)
+                   + (cfg.rays_background * cfg.points_per_ray * flop_per_sample(128)
+                      if cfg.train_background else 0))
+    kernel_ms = mlp_ms.value / max(n_launch.value, 1)
+    achieved = flop_launch / (kernel_ms * 1e-3) / 1e12
+    traffic = None
+    tf_path = ROOT / "profiles" / "traffic.json"
+    if tf_path.exists():
+        traffic = json.loads(tf_path.read_text()).get("mlp_kernel_dram_bytes_per_launch")
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, n, dt = cpu_sample(scene, args.cpu_seconds)
+        cores = blas_threads()
+        cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
+               "sample": f"{n} full map-update steps of config 2 ({dt*1e3:.0f} ms/step) through "
+                         f"oracle/vobj_oracle.py map_update_step (numpy/OpenBLAS, {cores} threads)"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": _config(world),
+            "samples_per_s": value * cfg.rays_per_object * cfg.points_per_ray,
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+            "gpu_launches": 4 * args.steps,
+            "roofline": {"bound": "fp32", "achieved": achieved, "peak": ffma_peak, "unit": "TFLOP/s",
+                         "frac": achieved / ffma_peak, "traffic": traffic, "kernel": "mlp_kernel (fused KF)",
+                         "kernel_ms": kernel_ms, "flop_per_launch": flop_launch,
+                         "peak_source": "FP32 FFMA throughput measured in this run by vm_ffma_peak "
+                                        "(MEASURED_PEAKS.json has no FP32 entry)"},
+            "clocks": clk.summary(),
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line))
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

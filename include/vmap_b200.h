@@ -102,11 +102,12 @@ typedef struct VmBatch {
 /* LossWeights (render.py:61-64). */
 typedef struct VmLossWeights { float colour, occupancy; } VmLossWeights;
 
-/* Status words written by vm_train_step (device int32[4*n_stacks], caller
-   zero-fills nothing: the call initialises them):
+/* Status words written by vm_train_step (device int32[4*n_stacks]; the call
+   initialises them to the sentinel 0x7f7f7f7f = "none"):
    [4s+0] first model index with a non-finite gradient among the models Adam
-          would update, or -1      (models.py:423-428 FloatingPointError)
-   [4s+1] first model index with a non-finite loss, or -1 (trainer.py:404-407)
+          would update, else sentinel (models.py:423-428 FloatingPointError)
+   [4s+1] first model index with a non-finite loss, else sentinel
+          (trainer.py:404-407)
    [4s+2] 1 if Adam ran for stack s, else 0
    [4s+3] reserved */
 
@@ -197,6 +198,12 @@ int vm_sample(const VmSampleObject* objects /* device [K] */, int n_objects,
               const VmKeyframe* keyframes /* device */, const float* rgbd /* float4 texels */,
               const uint8_t* mask, const VmSampleParams* params, VmBatch* out /* device ptrs */,
               VmSampleAux* aux, void* workspace, size_t workspace_bytes, void* stream);
+
+/* ---- profiling: event-time every fused-kernel launch of vm_train_step ---- */
+int vm_profile_enable(int on);                          /* resets the launch log */
+int vm_profile_read(int* launches, double* total_ms);   /* syncs on the events */
+/* CTA count and dynamic smem the fused kernel would use for these stacks. */
+int vm_train_grid(const VmStack* stacks, const VmBatch* batches, int n_stacks, int* ctas, int* smem_bytes);
 
 /* ---- misc ---------------------------------------------------------------- */
 const char* vm_last_error(void);

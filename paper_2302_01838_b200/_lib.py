@@ -99,6 +99,10 @@ _SIGNATURES = {
     "vm_sample": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
                             C.POINTER(VmSampleParams), C.POINTER(VmBatch), C.POINTER(VmSampleAux),
                             C.c_void_p, C.c_size_t, C.c_void_p]),
+    "vm_profile_enable": (C.c_int, [C.c_int]),
+    "vm_profile_read": (C.c_int, [C.POINTER(C.c_int), C.POINTER(C.c_double)]),
+    "vm_train_grid": (C.c_int, [C.POINTER(VmStack), C.POINTER(VmBatch), C.c_int, C.POINTER(C.c_int),
+                                C.POINTER(C.c_int)]),
     "vm_last_error": (C.c_char_p, []),
     "vm_version": (C.c_char_p, []),
     "vm_ffma_peak": (C.c_int, [C.c_int, C.POINTER(C.c_float), C.c_void_p]),

@@ -33,14 +33,44 @@ __device__ __forceinline__ void load_weights(const KStack& st, const float* __re
   }
 }
 
-// Load the block's encoded samples (feature-major) and t.
-__device__ __forceinline__ void load_block(const KStack& st, int64_t gs0, int ns, float* __restrict__ E,
+// Load the block's samples into E (feature-major) and t.  Encoded input is
+// transposed from [sample][D]; point input is encoded on the fly with
+// models.py:286-308's layout [p, sin(pi 2^i p / s) x3, cos(...) x3 per band]
+// (f32 sincospif: tolerance-level vs the reference's f64 encoding).
+__device__ __forceinline__ void load_block(const KStack& st, int k, int64_t gs0, int ns, float* __restrict__ E,
                                            float* __restrict__ tS, int tt, int nthr, bool with_t) {
   const int D = st.D;
-  const float* src = st.enc + gs0 * D;
-  for (int idx = tt; idx < kSB * D; idx += nthr) {
-    const int s = idx / D, f = idx - s * D;
-    E[f * kLD + s] = s < ns ? src[idx] : 0.f;
+  if (st.pts) {
+    const float scale = st.pe_scale[k];
+    for (int s = tt; s < kSB; s += nthr) {
+      float p[3] = {0.f, 0.f, 0.f};
+      if (s < ns) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) p[c] = st.pts[(gs0 + s) * 3 + c];
+      }
+      int f = 0;
+      if (st.include_input) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) E[c * kLD + s] = p[c];
+        f = 3;
+      }
+      for (int b = 0; b < st.n_freq; ++b, f += 6) {
+        const float coef = float(double(1u << b) / double(scale));
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          float sn, cs;
+          sincospif(coef * p[c], &sn, &cs);
+          E[(f + c) * kLD + s] = s < ns ? sn : 0.f;
+          E[(f + 3 + c) * kLD + s] = s < ns ? cs : 0.f;
+        }
+      }
+    }
+  } else {
+    const float* src = st.enc + gs0 * D;
+    for (int idx = tt; idx < kSB * D; idx += nthr) {
+      const int s = idx / D, f = idx - s * D;
+      E[f * kLD + s] = s < ns ? src[idx] : 0.f;
+    }
   }
   for (int idx = tt; idx < (st.Dp - D) * kSB; idx += nthr) E[(D + idx / kSB) * kLD + (idx % kSB)] = 0.f;
   if (with_t && tt < kSB) tS[tt] = tt < ns ? st.t[gs0 + tt] : 0.f;
@@ -96,7 +126,7 @@ __device__ void run_item(const KStack& st, int item, float* smem) {
       gs0 = gs_model + int64_t(blk) * kSB;
       { const int64_t rem = st.N - int64_t(blk) * kSB; ns = int(rem < kSB ? rem : kSB); }
     }
-    load_block(st, gs0, ns, E, tS, wt * 32 + lane, T * 32, MODE == kTrain);
+    load_block(st, k, gs0, ns, E, tS, wt * 32 + lane, T * 32, MODE == kTrain);
     team_sync(team, T);
 
     // ---------------- forward ----------------
@@ -477,6 +507,22 @@ static int choose_splits(const KStack* ks, int n, int* P) {
 using namespace vm;
 
 namespace {
+// Optional per-launch CUDA-event timing of the fused kernel (bench.py reads
+// it to report the kernel's roofline fraction from the timed region itself).
+struct KernelProfiler {
+  bool on = false;
+  std::vector<cudaEvent_t> ev;  // start/stop pairs
+  size_t used = 0;
+  cudaEvent_t get() {
+    if (used == ev.size()) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      ev.push_back(e);
+    }
+    return ev[used++];
+  }
+} g_prof;
+
 struct TrainPlan {
   KParams kp;
   AdamParams ap;
@@ -509,11 +555,16 @@ int plan_train(const VmStack* stacks, const VmBatch* batches, int n, TrainPlan& 
     VM_REQUIRE(b.n_models == stacks[i].count, "vm_train_step: batch leading axis != params.count");
     VM_REQUIRE(b.input_dim == stacks[i].arch.input_dim, "vm_train_step: encoding dim mismatch");
     VM_REQUIRE(b.n_points >= 1 && b.n_points <= kSB, "vm_train_step: points per ray must be in [1, 32]");
-    VM_REQUIRE(b.encoded != nullptr, "vm_train_step: encoded input required");
+    VM_REQUIRE(b.encoded != nullptr || (b.points != nullptr && b.pe_scale != nullptr),
+               "vm_train_step: encoded input or points + pe_scale required");
     ks.R = b.n_rays;
     ks.S = b.n_points;
     ks.G = kSB / b.n_points;
     ks.enc = b.encoded;
+    ks.pts = b.encoded ? nullptr : b.points;
+    ks.pe_scale = b.pe_scale;
+    ks.n_freq = (stacks[i].arch.input_dim % 6 == 3) ? (stacks[i].arch.input_dim - 3) / 6 : stacks[i].arch.input_dim / 6;
+    ks.include_input = stacks[i].arch.input_dim % 6 == 3;
     ks.t = b.t;
     ks.tdepth = b.target_depth;
     ks.tcol = b.target_colour;
@@ -572,6 +623,8 @@ extern "C" int vm_train_step(const VmStack* stacks, const VmBatch* batches, int 
   cudaStream_t s = cudaStream_t(stream);
   char* ws = static_cast<char*>(workspace);
   VM_CUDA(cudaMemsetAsync(status, 0x7f, sizeof(int32_t) * 4 * n_stacks, s));
+  for (int i = 0; i < n_stacks; ++i)  // last-CTA tickets (the workspace may have held another plan)
+    if (pl.kp.s[i].P > 1) VM_CUDA(cudaMemsetAsync(ws + pl.off_cnt[i], 0, size_t(pl.kp.s[i].K) * 4, s));
   int loss_off = 0;
   for (int i = 0; i < n_stacks; ++i) {
     KStack& ks = pl.kp.s[i];
@@ -604,8 +657,15 @@ extern "C" int vm_train_step(const VmStack* stacks, const VmBatch* batches, int 
     set_error("vm_train_step: no kernel for this architecture");
     return VM_ERR_UNSUPPORTED;
   }
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (g_prof.on) {
+    e0 = g_prof.get();
+    e1 = g_prof.get();
+    VM_CUDA(cudaEventRecord(e0, s));
+  }
   rc = launch_mlp(fn, pl.kp, pl.grid, pl.smem, s);
   if (rc) return rc;
+  if (g_prof.on) VM_CUDA(cudaEventRecord(e1, s));
   if (pl.adam_grid > 0) {
     adam_train_kernel<<<pl.adam_grid, 256, 0, s>>>(pl.ap);
     VM_CUDA(cudaGetLastError());
@@ -665,4 +725,33 @@ extern "C" int vm_backward(const VmStack* st, const float* encoded, int64_t n_sa
                            const float* grad_col, float* grads, void* stream) {
   return run_fwd_bwd(st, encoded, n_samples, grad_occ, grad_col, nullptr, nullptr, grads, true,
                      cudaStream_t(stream));
+}
+
+extern "C" int vm_profile_enable(int on) {
+  g_prof.on = on != 0;
+  g_prof.used = 0;
+  return VM_OK;
+}
+
+extern "C" int vm_profile_read(int* launches, double* total_ms) {
+  double t = 0.0;
+  for (size_t i = 0; i + 1 < g_prof.used; i += 2) {
+    VM_CUDA(cudaEventSynchronize(g_prof.ev[i + 1]));
+    float ms = 0.f;
+    VM_CUDA(cudaEventElapsedTime(&ms, g_prof.ev[i], g_prof.ev[i + 1]));
+    t += ms;
+  }
+  *launches = int(g_prof.used / 2);
+  *total_ms = t;
+  return VM_OK;
+}
+
+extern "C" int vm_train_grid(const VmStack* stacks, const VmBatch* batches, int n_stacks, int* ctas,
+                             int* smem_bytes) {
+  TrainPlan pl;
+  int rc = plan_train(stacks, batches, n_stacks, pl);
+  if (rc) return rc;
+  *ctas = pl.grid;
+  *smem_bytes = int(pl.smem);
+  return VM_OK;
 }

@@ -61,7 +61,10 @@ struct KStack {
   const float* corr1;
   const float* corr2;
   int corr_len;
-  const float* enc;
+  const float* enc;       // [K][R*S][D] encoded samples, or
+  const float* pts;       // [K][R*S][3] box-normalised points (PE fused here)
+  const float* pe_scale;  // [K] per-model PE scale (points path)
+  int n_freq, include_input;
   const float* t;
   const float* tdepth;
   const float* tcol;

@@ -1,0 +1,168 @@
+"""Device keyframe arena + the CUDA ray/sample generator (vm_sample).
+
+Keyframe crops (objects.py:86-93: rgb f32x3, depth f32, mask bool) are packed
+into one growing device arena of float4 RGBD texels plus a mask byte per
+texel, so every training ray's gather is one 16-B load and one byte
+(SURVEY 7 design notes).  Per-keyframe descriptors (bbox, pose, arena
+offset) and per-object descriptors (object id = RNG key part, padded box,
+PE scale) are small tables re-uploaded only when the map changes.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import torch
+
+from . import _lib
+from .models import DEVICE
+
+
+class KeyframeArena:
+    def __init__(self, device=DEVICE, capacity_texels: int = 1 << 20):
+        self.device = torch.device(device)
+        self.rgbd = torch.zeros((capacity_texels, 4), dtype=torch.float32, device=self.device)
+        self.mask = torch.zeros(capacity_texels, dtype=torch.uint8, device=self.device)
+        self.used = 0
+
+    def _reserve(self, n: int) -> None:
+        need = self.used + n
+        cap = self.rgbd.shape[0]
+        if need <= cap:
+            return
+        while cap < need:
+            cap *= 2
+        rgbd = torch.zeros((cap, 4), dtype=torch.float32, device=self.device)
+        mask = torch.zeros(cap, dtype=torch.uint8, device=self.device)
+        rgbd[:self.used] = self.rgbd[:self.used]
+        mask[:self.used] = self.mask[:self.used]
+        self.rgbd, self.mask = rgbd, mask
+
+    def add(self, kf) -> int:
+        """Upload one Keyframe's crops; records kf.texel_off and returns it."""
+        u0, v0, u1, v1 = kf.bbox
+        h, w = v1 - v0, u1 - u0
+        if kf.rgb.shape[:2] != (h, w) or kf.depth.shape != (h, w) or kf.mask.shape != (h, w):
+            raise ValueError(f"keyframe crop shapes do not match bbox {kf.bbox}")
+        n = h * w
+        self._reserve(n)
+        tex = np.empty((n, 4), np.float32)
+        tex[:, :3] = kf.rgb.reshape(n, 3)
+        tex[:, 3] = kf.depth.reshape(n)
+        off = self.used
+        self.rgbd[off:off + n] = torch.from_numpy(tex).to(self.device)
+        self.mask[off:off + n] = torch.from_numpy(kf.mask.reshape(n).astype(np.uint8)).to(self.device)
+        self.used += n
+        kf.texel_off = off
+        return off
+
+
+def _kf_desc(kf) -> _lib.VmKeyframe:
+    d = _lib.VmKeyframe()
+    d.texel_off = int(kf.texel_off)
+    d.u0, d.v0, d.u1, d.v1 = (int(x) for x in kf.bbox)
+    pose = np.asarray(kf.pose, np.float64)
+    for i in range(3):
+        for j in range(4):
+            d.pose[4 * i + j] = float(pose[i, j])
+    return d
+
+
+def build_tables(arena: KeyframeArena, instances, bound_pad: float, frozen=None, device=DEVICE):
+    """(keyframe table, object table) device byte tensors for instances in
+    model-index order.  Each instance's keyframes are laid out contiguously;
+    inactive / frozen / keyframe-less instances get a zero batch
+    (trainer.py:272-273, :336-338).  Crops not yet in the arena are uploaded."""
+    kfs = []
+    objs = (_lib.VmSampleObject * max(len(instances), 1))()
+    for k, inst in enumerate(instances):
+        o = objs[k]
+        o.object_id = int(inst.object_id)
+        o.kf_begin = len(kfs)
+        for kf in inst.keyframes:
+            if getattr(kf, "texel_off", -1) < 0:
+                arena.add(kf)
+            kfs.append(_kf_desc(kf))
+        o.n_kf = len(inst.keyframes)
+        live = bool(inst.active) and not (frozen is not None and bool(frozen[k]))
+        o.active = 1 if live else 0
+        box = inst.aabb.padded(bound_pad)        # geometry.py:40-42
+        c, h = box.center, box.half_extent
+        for i in range(3):
+            o.box_min[i], o.box_max[i] = float(box.min[i]), float(box.max[i])
+            o.center[i], o.half[i] = float(c[i]), float(h[i])
+        o.pe_scale = float(inst.pe_scale)
+    kf_arr = (_lib.VmKeyframe * max(len(kfs), 1))(*kfs) if kfs else (_lib.VmKeyframe * 1)()
+    to_dev = lambda a: torch.from_numpy(np.frombuffer(bytes(a), dtype=np.uint8).copy()).to(device)
+    return to_dev(kf_arr), to_dev(objs)
+
+
+def sample_params(intr, sampling, seed: int, step: int, n_rays: int, arch, encode: bool) -> _lib.VmSampleParams:
+    p = _lib.VmSampleParams()
+    p.seed, p.step, p.n_rays = int(seed), int(step), int(n_rays)
+    p.n_stratified, p.n_surface = sampling.n_stratified, sampling.n_surface
+    p.encode = 1 if encode else 0
+    p.n_freq, p.include_input = arch.n_freq, 1 if arch.include_input else 0
+    p.fx, p.fy, p.cx, p.cy = float(intr.fx), float(intr.fy), float(intr.cx), float(intr.cy)
+    p.width, p.height = int(intr.width), int(intr.height)
+    p.t_near, p.t_far = float(sampling.t_near), float(sampling.t_far)
+    p.surface_std = float(sampling.surface_std)
+    p.three_std = 3.0 * float(sampling.surface_std)   # python f64, as render.py:200/211 forms it
+    return p
+
+
+class SampleBuffers:
+    """Persistent device outputs of one vm_sample call (one stack)."""
+
+    def __init__(self, K: int, R: int, S: int, D: int, encode: bool, device, aux: bool = False):
+        f = lambda *s: torch.zeros(s, dtype=torch.float32, device=device)
+        b = lambda *s: torch.zeros(s, dtype=torch.bool, device=device)
+        self.K, self.R, self.S, self.D, self.encode = K, R, S, D, encode
+        self.encoded = f(K, R, S, D) if encode else None
+        self.points = None if encode else f(K, R, S, 3)
+        self.pe_scale = f(max(K, 1))
+        self.t = f(K, R, S)
+        self.target_depth = f(K, R)
+        self.target_colour = f(K, R, 3)
+        self.target_mask = b(K, R)
+        self.valid_depth = b(K, R)
+        self.ray_ok = b(K, R)
+        self.aux = None
+        if aux:
+            i64 = lambda *s: torch.zeros(s, dtype=torch.int64, device=device)
+            self.aux = dict(kf_idx=i64(K, R), u=i64(K, R), v=i64(K, R),
+                            t64=torch.zeros((K, R, S), dtype=torch.float64, device=device))
+        self.ws = None
+        self.obj_dev = None
+
+    def vm(self) -> _lib.VmBatch:
+        out = _lib.VmBatch()
+        out.n_models, out.n_rays, out.n_points, out.input_dim = self.K, self.R, self.S, self.D
+        out.encoded = _lib.ptr(self.encoded)
+        out.points = _lib.ptr(self.points)
+        out.pe_scale = self.pe_scale.data_ptr()
+        out.t = self.t.data_ptr()
+        out.target_depth = self.target_depth.data_ptr()
+        out.target_colour = self.target_colour.data_ptr()
+        out.target_mask = self.target_mask.data_ptr()
+        out.valid_depth = self.valid_depth.data_ptr()
+        out.ray_ok = self.ray_ok.data_ptr()
+        return out
+
+
+def run_sampler(arena: KeyframeArena, kf_table: torch.Tensor, obj_table: torch.Tensor, n_objects: int,
+                params: _lib.VmSampleParams, buf: SampleBuffers) -> None:
+    lib = _lib.load()
+    nbytes = lib.vm_sample_workspace_bytes(n_objects, C.byref(params))
+    if buf.ws is None or buf.ws.numel() < nbytes:
+        buf.ws = torch.zeros(max(nbytes, 256), dtype=torch.uint8, device=arena.device)
+    batch = buf.vm()
+    aux = None
+    if buf.aux is not None:
+        aux = _lib.VmSampleAux(buf.aux["kf_idx"].data_ptr(), buf.aux["u"].data_ptr(), buf.aux["v"].data_ptr(),
+                               buf.aux["t64"].data_ptr())
+    _lib.check(lib.vm_sample(obj_table.data_ptr(), n_objects, kf_table.data_ptr(),
+                             arena.rgbd.data_ptr(), arena.mask.data_ptr(), C.byref(params), C.byref(batch),
+                             C.byref(aux) if aux is not None else None, buf.ws.data_ptr(), buf.ws.numel(),
+                             _lib.stream_ptr()), "vm_sample")

@@ -284,12 +284,14 @@ def _grow(params: StackedModelParams, state: OptimState, min_capacity: int) -> N
 
 
 def append_model(params: StackedModelParams, state: OptimState, seed: int,
-                 stream: int = PURPOSE_INIT_OBJECT) -> int:
-    """models.py:253-277."""
+                 stream: int = PURPOSE_INIT_OBJECT, init_index: int | None = None) -> int:
+    """models.py:253-277.  ``init_index`` (default: the new slot) is the model
+    index the init stream is keyed by; object-sharded ranks pass the object's
+    global append index so their weights equal a single-stack run's."""
     idx = params.count
     if idx + 1 > params.capacity:
         _grow(params, state, idx + 1)
-    ws, bs = _init_model_arrays(params.arch, seed, idx, stream)
+    ws, bs = _init_model_arrays(params.arch, seed, idx if init_index is None else init_index, stream)
     blk = params._layout.pack([w[None] for w in ws], [b[None] for b in bs])[0]
     params.arena[idx] = torch.from_numpy(blk).to(params.arena.device)
     state.m_arena[idx] = 0

@@ -45,7 +45,7 @@ class Keyframe:
     mask: np.ndarray
     rgb: np.ndarray
     depth: np.ndarray
-    arena_slot: int = -1
+    texel_off: int = -1  # offset of the crop in the device texel arena (-1: not uploaded)
 
 
 @dataclass

@@ -1,0 +1,134 @@
+"""Object-parallel multi-GPU plumbing.
+
+Every object is an independent model with its own keyframes, RNG streams
+(keyed by object id) and Adam state, so objects shard across ranks with no
+gradient collective.  What crosses ranks:
+  * per step: the per-object loss triples (+ object ids) -> one all_gather
+    (NCCL over NVLink on GPUs, gloo in the CPU tests);
+  * on rebalance: an object's parameter block + Adam moments + step counter
+    (point-to-point send/recv of one packed tensor).
+Placement is longest-processing-time greedy on a per-object cost (rays x
+samples x FLOP/sample), so a heavy background model gets its own share.
+Model initialisation keys stay the object's global append index (SURVEY 8e
+"init-key caveat"), so a sharded run starts from the same weights as a
+single-stack run.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+
+def plan_by_cost(costs, world: int) -> list[int]:
+    """LPT greedy: returns owner rank per item (deterministic tie-breaks)."""
+    order = sorted(range(len(costs)), key=lambda i: (-float(costs[i]), i))
+    load = [0.0] * world
+    owner = [0] * len(costs)
+    for i in order:
+        r = min(range(world), key=lambda q: (load[q], q))
+        owner[i] = r
+        load[r] += float(costs[i])
+    return owner
+
+
+def object_cost(rays: int, points: int, hidden: int, input_dim: int = 33) -> float:
+    mac_fwd = hidden * input_dim + 2 * hidden * hidden + 4 * hidden
+    mac_dx = 2 * hidden * hidden + 4 * hidden
+    return float(rays * points * 2 * (2 * mac_fwd + mac_dx))
+
+
+@dataclass
+class ObjectSharding:
+    world: int
+    owner: list            # owner rank per global object index
+    background_rank: int = 0
+    _gather_buf: torch.Tensor | None = field(default=None, repr=False)
+
+    @staticmethod
+    def plan(scene: dict, world: int, rays_object: int = 120, rays_background: int = 1200, points: int = 10,
+             hidden_object: int = 32, hidden_background: int = 128) -> "ObjectSharding":
+        n = len(scene["objects"])
+        costs = [object_cost(rays_object, points, hidden_object)] * n
+        bg = scene.get("background") is not None
+        if bg:
+            costs = costs + [object_cost(rays_background, points, hidden_background)]
+        owner = plan_by_cost(costs, world) if world > 1 else [0] * len(costs)
+        bg_rank = owner[-1] if bg else 0
+        return ObjectSharding(world, owner[:n], bg_rank)
+
+    def objects_of(self, rank: int) -> list[int]:
+        return [i for i, r in enumerate(self.owner) if r == rank]
+
+    # -------------------------------------------------------- loss gather
+    def gather_losses_device(self, losses: torch.Tensor) -> torch.Tensor | None:
+        """All-gather a [k_local, 3] loss tensor (padded to the max shard) on the
+        current stream; no host sync.  Returns the gathered [world, kmax, 3]."""
+        if self.world == 1:
+            return None
+        import torch.distributed as dist
+        kmax = max(sum(1 for r in self.owner if r == q) for q in range(self.world)) + 1
+        if self._gather_buf is None or self._gather_buf.shape[1] != kmax or self._gather_buf.device != losses.device:
+            self._gather_buf = torch.zeros((self.world, kmax, 3), dtype=losses.dtype, device=losses.device)
+            self._send = torch.zeros((kmax, 3), dtype=losses.dtype, device=losses.device)
+        self._send.zero_()
+        self._send[:losses.shape[0]] = losses
+        dist.all_gather_into_tensor(self._gather_buf.view(-1), self._send.view(-1))
+        return self._gather_buf
+
+    def gather_losses(self, report) -> dict | None:
+        """Host-level gather of StepReport.losses (object id -> triple) to every
+        rank; returns the merged dict."""
+        if self.world == 1:
+            return dict(report.losses)
+        import torch.distributed as dist
+        ids = sorted(report.losses)
+        kmax = max(sum(1 for r in self.owner if r == q) for q in range(self.world)) + 1
+        dev = torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available() else torch.device("cpu")
+        send = torch.full((kmax, 4), -1.0, dtype=torch.float64, device=dev)
+        for j, oid in enumerate(ids):
+            send[j, 0] = oid
+            send[j, 1:] = torch.tensor(report.losses[oid], dtype=torch.float64)
+        out = torch.empty((self.world * kmax, 4), dtype=torch.float64, device=dev)
+        dist.all_gather_into_tensor(out, send)
+        merged = {}
+        for row in out.cpu().numpy():
+            if row[0] >= 0:
+                merged[int(row[0])] = (float(row[1]), float(row[2]), float(row[3]))
+        return merged
+
+
+# ------------------------------------------------------------ migration
+
+
+def pack_model(arena: torch.Tensor, m: torch.Tensor, v: torch.Tensor, step: torch.Tensor, k: int) -> torch.Tensor:
+    """One object's parameter block, Adam moments and step counter as a flat
+    float32 tensor (step stored as two exact float32 halves)."""
+    s = int(step[k].item())
+    meta = torch.tensor([float(s & 0xFFFFFF), float(s >> 24)], dtype=torch.float32, device=arena.device)
+    return torch.cat([arena[k], m[k], v[k], meta])
+
+
+def unpack_model(buf: torch.Tensor, arena: torch.Tensor, m: torch.Tensor, v: torch.Tensor, step: torch.Tensor,
+                 k: int) -> None:
+    b = arena.shape[1]
+    arena[k] = buf[:b]
+    m[k] = buf[b:2 * b]
+    v[k] = buf[2 * b:3 * b]
+    lo, hi = (int(x) for x in buf[3 * b:3 * b + 2].tolist())
+    step[k] = lo + (hi << 24)
+
+
+def migrate(arena, m, v, step, k_src: int, src: int, dst: int, rank: int, k_dst: int | None = None) -> None:
+    """Move model `k_src` of rank `src` into slot `k_dst` of rank `dst`
+    (point-to-point; collective over the pair)."""
+    import torch.distributed as dist
+    b = arena.shape[1]
+    if rank == src:
+        dist.send(pack_model(arena, m, v, step, k_src).contiguous(), dst)
+    elif rank == dst:
+        buf = torch.empty(3 * b + 2, dtype=torch.float32, device=arena.device)
+        dist.recv(buf, src)
+        unpack_model(buf, arena, m, v, step, k_src if k_dst is None else k_dst)

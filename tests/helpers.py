@@ -39,6 +39,82 @@ def assert_params_close(params, ost: O.Stack, rtol=1e-4, atol=1e-5, rel_l2=1e-4)
     assert rel.max() <= rel_l2, f"per-object relative L2 {rel.max():.3e} > {rel_l2}"
 
 
+def flat_params(params):
+    W, B = host_layers(params)
+    k = params.count
+    return np.concatenate([np.concatenate([W[l].reshape(k, -1), B[l]], 1) for l in range(len(W))],
+                          1).astype(np.float64)
+
+
+def flat_oracle(st: O.Stack):
+    k = st.count
+    return np.concatenate([np.concatenate([st.W[l][:k].reshape(k, -1), st.b[l][:k]], 1)
+                           for l in range(len(st.W))], 1).astype(np.float64)
+
+
+def f64_stack(st: O.Stack) -> O.Stack:
+    c = st.copy()
+    for name in ("W", "b", "mW", "vW", "mb", "vb"):
+        setattr(c, name, [a.astype(np.float64) for a in getattr(c, name)])
+    return c
+
+
+def f64_batch(hb: dict) -> dict:
+    return {k: (v.astype(np.float64) if v.dtype == np.float32 else v) for k, v in hb.items()}
+
+
+def rel_l2(a, b):
+    return np.linalg.norm(a - b, axis=1) / np.maximum(np.linalg.norm(b, axis=1), 1e-30)
+
+
+def assert_as_close_to_truth(gpu_flat, ref_flat, truth_flat, factor=2.0, floor=1e-4):
+    """Chaotic-drift contract: the GPU trajectory is no further (per object,
+    relative L2) from the f64 trajectory than `factor` x the f32 reference's
+    own distance, or within `floor`."""
+    e_gpu = rel_l2(gpu_flat, truth_flat)
+    e_ref = rel_l2(ref_flat, truth_flat)
+    bound = np.maximum(factor * e_ref, floor)
+    assert np.all(e_gpu <= bound), f"relL2 to f64: gpu {e_gpu.max():.3e} vs reference {e_ref.max():.3e}"
+
+
 def to_host_batch(b):
     return {k: getattr(b, k).cpu().numpy() for k in
             ("encoded", "t", "target_depth", "target_colour", "target_mask", "valid_depth", "ray_ok")}
+
+
+class _NS:
+    def __init__(self, **kw):
+        self.__dict__.update(kw)
+
+
+def oracle_mapstate(scene, cfg, obj_hidden=32, bg_hidden=128):
+    """Oracle MapState populated from a scenes.make_scene dict (same init keys
+    as Mapper: append order, PURPOSE_INIT_OBJECT / PURPOSE_INIT_BACKGROUND)."""
+    intr = scene["intrinsics"]
+
+    def kfs(spec):
+        out = []
+        for kf in spec["keyframes"]:
+            u0, v0, u1, v1 = kf["bbox"]
+            out.append(_NS(bbox=kf["bbox"], pose=np.asarray(kf["pose"], np.float64), mask=kf["mask"],
+                           rgb=scene["rgb"][v0:v1, u0:u1].astype(np.float32),
+                           depth=scene["depth"][v0:v1, u0:u1].astype(np.float32)))
+        return out
+
+    ao = O.Arch(cfg.arch_object.n_layers, cfg.arch_object.hidden, cfg.arch_object.n_freq)
+    ab = O.Arch(cfg.arch_background.n_layers, cfg.arch_background.hidden, cfg.arch_background.n_freq)
+    objs = []
+    for i, spec in enumerate(scene["objects"]):
+        objs.append(_NS(object_id=i + 1, keyframes=kfs(spec), aabb=spec["aabb"], pe_scale=cfg.pe_scale_object,
+                        active=True, model_index=i))
+    bg = None
+    if scene["background"] is not None:
+        bg = _NS(object_id=0, keyframes=kfs(scene["background"]), aabb=scene["background"]["aabb"],
+                 pe_scale=cfg.pe_scale_background, active=True, model_index=0)
+    ost = O.new_stack(ao, len(objs), cfg.seed, O.INIT_OBJECT)
+    bst = O.new_stack(ab, 1 if bg else 0, cfg.seed, O.INIT_BACKGROUND)
+    samp = O.Sampling(cfg.sampling.t_near, cfg.sampling.t_far, cfg.sampling.n_stratified,
+                      cfg.sampling.n_surface, cfg.sampling.surface_std)
+    return O.MapState(intr=intr, objects=objs, background=bg, obj=ost, bg=bst, seed=cfg.seed,
+                      rays_object=cfg.rays_per_object, rays_background=cfg.rays_background, sampling=samp,
+                      bound_pad=cfg.association.bound_pad, train_background=cfg.train_background)

@@ -75,7 +75,7 @@ class ObjectSharding:
             self._send = torch.zeros((kmax, 3), dtype=losses.dtype, device=losses.device)
         self._send.zero_()
         self._send[:losses.shape[0]] = losses
-        dist.all_gather_into_tensor(self._gather_buf.view(-1), self._send.view(-1))
+        _all_gather(self._gather_buf.view(self.world, -1), self._send.view(-1))
         return self._gather_buf
 
     def gather_losses(self, report) -> dict | None:
@@ -86,18 +86,30 @@ class ObjectSharding:
         import torch.distributed as dist
         ids = sorted(report.losses)
         kmax = max(sum(1 for r in self.owner if r == q) for q in range(self.world)) + 1
-        dev = torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available() else torch.device("cpu")
+        import torch.distributed as dist
+        dev = (torch.device("cuda", torch.cuda.current_device()) if dist.get_backend() == "nccl"
+               else torch.device("cpu"))
         send = torch.full((kmax, 4), -1.0, dtype=torch.float64, device=dev)
         for j, oid in enumerate(ids):
             send[j, 0] = oid
             send[j, 1:] = torch.tensor(report.losses[oid], dtype=torch.float64)
         out = torch.empty((self.world * kmax, 4), dtype=torch.float64, device=dev)
-        dist.all_gather_into_tensor(out, send)
+        _all_gather(out.view(self.world, -1), send.view(-1))
         merged = {}
         for row in out.cpu().numpy():
             if row[0] >= 0:
                 merged[int(row[0])] = (float(row[1]), float(row[2]), float(row[3]))
         return merged
+
+
+def _all_gather(out2d: torch.Tensor, send: torch.Tensor) -> None:
+    """out2d[r] <- send of rank r (NCCL all_gather_into_tensor; list form on gloo)."""
+    import torch.distributed as dist
+    if dist.get_backend() == "nccl":
+        dist.all_gather_into_tensor(out2d.view(-1), send)
+    else:
+        parts = list(out2d.unbind(0))
+        dist.all_gather(parts, send)
 
 
 # ------------------------------------------------------------ migration

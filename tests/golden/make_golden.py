@@ -1,0 +1,172 @@
+"""Generate golden vectors by running the REAL reference (`vobj`) in the build
+container.  /root/reference does not exist on the GPU box, so the outputs are
+committed as small .npz fixtures next to this script.
+
+The reference imports scikit-image (meshing) which is not installed; the hot
+path never calls it, so a stub module is injected first.
+
+    python tests/golden/make_golden.py          # rewrites tests/golden/*.npz
+"""
+
+from __future__ import annotations
+
+import sys
+import types
+from pathlib import Path
+
+import numpy as np
+
+HERE = Path(__file__).resolve().parent
+ROOT = HERE.parents[1]
+REF = Path("/root/reference/pkg/src")
+
+
+def import_reference():
+    sk = types.ModuleType("skimage")
+    sk.__version__ = "stub"
+    meas = types.ModuleType("skimage.measure")
+    meas.marching_cubes = lambda *a, **k: (_ for _ in ()).throw(RuntimeError("skimage stub"))
+    met = types.ModuleType("skimage.metrics")
+    met.structural_similarity = lambda *a, **k: 0.0
+    sk.measure, sk.metrics = meas, met
+    sys.modules.update({"skimage": sk, "skimage.measure": meas, "skimage.metrics": met})
+    sys.path.insert(0, str(REF))
+    import vobj  # noqa: F401
+    return vobj
+
+
+def ref_mapper(vobj, scene, rays_obj=120, rays_bg=1200, seed=0, train_bg=True):
+    from vobj import trainer as T
+    from vobj.geometry import AABB
+    from vobj.models import append_model
+    from vobj.objects import add_keyframe
+    from vobj.rng import PURPOSE_INIT_BACKGROUND, PURPOSE_INIT_OBJECT
+    from vobj.render import CameraIntrinsics
+    intr = scene["intrinsics"]
+    ri = CameraIntrinsics(intr.fx, intr.fy, intr.cx, intr.cy, intr.width, intr.height)
+    cfg = T.apply_config_overrides(T.TrainConfig(), {"seed": str(seed), "rays_per_object": str(rays_obj),
+                                                     "rays_background": str(rays_bg),
+                                                     "train_background": "1" if train_bg else "0"})
+    m = T.Mapper(ri, cfg)
+    if scene["background"] is not None:
+        b = scene["background"]
+        idx = append_model(m.bg_params, m.bg_state, cfg.seed, PURPOSE_INIT_BACKGROUND)
+        inst = m.map.add_background(AABB(b["aabb"].min, b["aabb"].max), cfg.pe_scale_background, idx)
+        for kf in b["keyframes"]:
+            add_keyframe(inst, kf["frame_id"], kf["pose"], kf["bbox"], kf["mask"], scene["rgb"], scene["depth"])
+    for ob in scene["objects"]:
+        idx = append_model(m.obj_params, m.obj_state, cfg.seed, PURPOSE_INIT_OBJECT)
+        inst = m.map.add_object(1, AABB(ob["aabb"].min, ob["aabb"].max), cfg.pe_scale_object, idx)
+        m.model_to_object.append(inst.object_id)
+        for kf in ob["keyframes"]:
+            add_keyframe(inst, kf["frame_id"], kf["pose"], kf["bbox"], kf["mask"], scene["rgb"], scene["depth"])
+    return m
+
+
+def flat(params):
+    k = params.count
+    return np.concatenate([np.concatenate([params.weights[l][:k].reshape(k, -1), params.biases[l][:k]], 1)
+                           for l in range(len(params.weights))], 1)
+
+
+def main():
+    vobj = import_reference()
+    from vobj import models as M
+    from vobj import render as Rn
+    from vobj import trainer as T
+    from vobj.objects import sample_training_pixels
+    sys.path.insert(0, str(ROOT))
+    from paper_2302_01838_b200.scenes import config, make_scene
+
+    out = {}
+    # ---- models: init, forward, backward, adam (models.py) ----------------
+    g = np.random.default_rng(123)
+    for tag, arch, k in (("h32", M.ModelArch(4, 32, 5), 3), ("h16l3", M.ModelArch(3, 16, 3), 2)):
+        p, s = M.init_stacked(arch, k, seed=42)
+        out[f"{tag}_init"] = flat(p)
+        enc = g.uniform(-1, 1, (k, 57, arch.input_dim)).astype(np.float32)
+        fo, cache = M.forward(p, enc)
+        go = g.standard_normal((k, 57)).astype(np.float32)
+        gc = g.standard_normal((k, 57, 3)).astype(np.float32)
+        gr = M.backward(p, cache, go, gc)
+        out[f"{tag}_enc"], out[f"{tag}_go"], out[f"{tag}_gc"] = enc, go, gc
+        out[f"{tag}_occ"], out[f"{tag}_col"] = fo.occupancy, fo.colour
+        out[f"{tag}_dW"] = np.concatenate([np.concatenate([gr.d_weights[l].reshape(k, -1), gr.d_biases[l]], 1)
+                                           for l in range(arch.n_layers)], 1)
+        mask = np.array([True, False, True][:k])
+        M.set_frozen(p, 0, k > 2)
+        for _ in range(3):
+            M.adam_step(p, s, gr, update_mask=mask)
+        out[f"{tag}_adam3"] = flat(p)
+        out[f"{tag}_adam3_step"] = s.step[:k].copy()
+    # ---- render + losses (render.py) ---------------------------------------
+    R, S = 64, 10
+    occ = g.uniform(0, 1, (R, S)).astype(np.float32)
+    occ[0, 1] = 1.0
+    col = g.uniform(0, 1, (R, S, 3)).astype(np.float32)
+    t = np.sort(g.uniform(0.1, 8, (R, S)), axis=1).astype(np.float32)
+    res = Rn.render_rays(occ, col, t)
+    gO, gD, gC = (g.standard_normal(R).astype(np.float32), g.standard_normal(R).astype(np.float32),
+                  g.standard_normal((R, 3)).astype(np.float32))
+    d_occ, d_col = Rn.render_backward(occ, col, t, res, gO, gD, gC)
+    out.update(r_occ=occ, r_col=col, r_t=t, r_O=res.opacity, r_D=res.depth, r_C=res.colour, r_w=res.weights,
+               r_T=res.transmittance, r_gO=gO, r_gD=gD, r_gC=gC, r_docc=d_occ, r_dcol=d_col)
+    tD = g.uniform(0, 4, R).astype(np.float32)
+    tC = g.uniform(0, 1, (R, 3)).astype(np.float32)
+    tm, tv, tok = g.random(R) < 0.6, g.random(R) < 0.8, g.random(R) < 0.9
+    ld, lc, lo, lt = Rn.compute_losses(res, tD, tC, tm, tv, tok, Rn.LossWeights())
+    dO, dD, dC = Rn.loss_output_grads(res, tD, tC, tm, tv, tok, Rn.LossWeights())
+    out.update(l_tD=tD, l_tC=tC, l_m=tm, l_v=tv, l_ok=tok, l_ld=ld, l_lc=lc, l_lo=lo, l_lt=lt, l_dO=dO, l_dD=dD,
+               l_dC=dC)
+    np.savez_compressed(HERE / "ops.npz", **out)
+
+    # ---- sampler + map-update on config 1 (trainer.py / objects.py) ---------
+    scene = config("1")
+    m = ref_mapper(vobj, scene)
+    samp = {}
+    for step in (0, 3):
+        for k in range(m.obj_params.count):
+            inst = m.instance_for_model(k)
+            kf, u, v, hit = sample_training_pixels(inst, m.cfg.seed, step, m.cfg.rays_per_object)
+            b = m._assemble_batch(inst, m.cfg.rays_per_object, step)
+            pre = f"s{step}_o{k}_"
+            samp.update({pre + "kf": kf, pre + "u": u, pre + "v": v, pre + "mask": hit, pre + "t": b.t,
+                         pre + "ok": b.ray_ok, pre + "tdepth": b.target_depth, pre + "tcol": b.target_colour,
+                         pre + "valid": b.valid_depth})
+            if step == 0:
+                samp[pre + "enc"] = b.encoded
+        bg = m.map.background
+        b = m._assemble_batch(bg, m.cfg.rays_background, step)
+        pre = f"s{step}_bg_"
+        samp.update({pre + "t": b.t, pre + "ok": b.ray_ok, pre + "tdepth": b.target_depth, pre + "tmask": b.target_mask})
+        if step == 0:
+            samp[pre + "enc200"] = b.encoded[:200]
+    np.savez_compressed(HERE / "sampler_cfg1.npz", **samp)
+
+    tr = {}
+    losses = []
+    for step in range(20):
+        rep = m.train_step()
+        losses.append([rep.losses[oid] for oid in sorted(rep.losses)])
+    tr["losses"] = np.array(losses, np.float64)        # [20, 1+K, 3] sorted by object id (0 = bg)
+    tr["obj_params"] = flat(m.obj_params)
+    tr["bg_params"] = flat(m.bg_params)
+    # the reference's own benchmark input (trainer.py:594-606) through train_on_batch
+    for tag, arch, k, rays, pts in (("syn32", M.ModelArch(4, 32, 5), 5, 120, 10),
+                                    ("syn16", M.ModelArch(3, 16, 3), 3, 24, 6)):
+        p, s = M.init_stacked(arch, k, seed=11)
+        batch = T._synthetic_batch(arch, k, rays, pts, seed=7)
+        ls = [T.train_on_batch(p, s, batch, Rn.LossWeights()) for _ in range(20)]
+        tr[f"{tag}_losses"] = np.array(ls)
+        tr[f"{tag}_params"] = flat(p)
+    np.savez_compressed(HERE / "train_cfg1.npz", **tr)
+    import numpy
+    (HERE / "PROVENANCE.txt").write_text(
+        "Generated by tests/golden/make_golden.py from the reference at /root/reference/pkg/src\n"
+        f"numpy {numpy.__version__}; scipy {__import__('scipy').__version__}\n")
+    for f in ("ops.npz", "sampler_cfg1.npz", "train_cfg1.npz"):
+        print(f, (HERE / f).stat().st_size)
+
+
+if __name__ == "__main__":
+    main()

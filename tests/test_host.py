@@ -66,7 +66,7 @@ def test_lpt_plan_balances_and_is_deterministic():
     # LPT bound: makespan <= max(largest item, 4/3 x ideal); the background
     # (125 objects' worth of FLOPs) is indivisible and gets a rank of its own
     assert max(load) <= max(max(costs), 4 / 3 * sum(costs) / 4) * (1 + 1e-9)
-    assert sorted(load)[0] == sorted(load)[2]   # the object-only ranks are level
+    assert sorted(load)[2] - sorted(load)[0] <= costs[0]   # object-only ranks level within one object
     sh = ObjectSharding.plan(make_scene(20, n_kf=1, width=64, height=48, focal=40, crop=(10, 20)), 3)
     assert sorted(sum((sh.objects_of(r) for r in range(3)), [])) == list(range(20))
 

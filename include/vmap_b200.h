@@ -185,6 +185,10 @@ typedef struct VmSampleParams {
   double fx, fy, cx, cy;
   int32_t width, height;
   double t_near, t_far, surface_std, three_std; /* three_std = 3.0*surface_std (python f64) */
+  /* If non-NULL the RNG step key is (*step_dev + step_offset) read on the
+     device (CUDA-graph replay); otherwise `step`. */
+  const int64_t* step_dev;
+  int64_t step_offset;
 } VmSampleParams;
 
 /* Debug/parity outputs of the sampler (optional, may be NULL). */
@@ -202,8 +206,13 @@ int vm_sample(const VmSampleObject* objects /* device [K] */, int n_objects,
 /* ---- profiling: event-time every fused-kernel launch of vm_train_step ---- */
 int vm_profile_enable(int on);                          /* resets the launch log */
 int vm_profile_read(int* launches, double* total_ms);   /* syncs on the events */
+int vm_profile_kernels(long* n);                        /* kernels launched since enable */
+void vm_profile_count_kernels(int n);                   /* internal: launch counter */
 /* CTA count and dynamic smem the fused kernel would use for these stacks. */
 int vm_train_grid(const VmStack* stacks, const VmBatch* batches, int n_stacks, int* ctas, int* smem_bytes);
+
+/* Device step counter used by graph-replayed steps: *counter += inc. */
+int vm_step_advance(int64_t* counter, int64_t inc, void* stream);
 
 /* ---- misc ---------------------------------------------------------------- */
 const char* vm_last_error(void);

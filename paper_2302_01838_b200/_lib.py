@@ -74,7 +74,7 @@ class VmSampleParams(C.Structure):
                 ("fx", C.c_double), ("fy", C.c_double), ("cx", C.c_double), ("cy", C.c_double),
                 ("width", C.c_int32), ("height", C.c_int32),
                 ("t_near", C.c_double), ("t_far", C.c_double), ("surface_std", C.c_double),
-                ("three_std", C.c_double)]
+                ("three_std", C.c_double), ("step_dev", C.c_void_p), ("step_offset", C.c_int64)]
 
 
 class VmSampleAux(C.Structure):
@@ -101,8 +101,11 @@ _SIGNATURES = {
                             C.c_void_p, C.c_size_t, C.c_void_p]),
     "vm_profile_enable": (C.c_int, [C.c_int]),
     "vm_profile_read": (C.c_int, [C.POINTER(C.c_int), C.POINTER(C.c_double)]),
+    "vm_profile_kernels": (C.c_int, [C.POINTER(C.c_long)]),
+    "vm_profile_count_kernels": (None, [C.c_int]),
     "vm_train_grid": (C.c_int, [C.POINTER(VmStack), C.POINTER(VmBatch), C.c_int, C.POINTER(C.c_int),
                                 C.POINTER(C.c_int)]),
+    "vm_step_advance": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p]),
     "vm_last_error": (C.c_char_p, []),
     "vm_version": (C.c_char_p, []),
     "vm_ffma_peak": (C.c_int, [C.c_int, C.POINTER(C.c_float), C.c_void_p]),

@@ -76,6 +76,116 @@ __device__ __forceinline__ void load_block(const KStack& st, int k, int64_t gs0,
   if (with_t && tt < kSB) tS[tt] = tt < ns ? st.t[gs0 + tt] : 0.f;
 }
 
+// Per-model epilogue of a training step: update mask = ray_ok.any(-1)
+// (trainer.py:504) and active = !frozen; the model's loss triple as numpy's
+// pairwise sum over rays of the per-ray terms (render.py:305-307); the
+// non-finite flags Adam and the host need (models.py:423-428,
+// trainer.py:404-407); this step's bias corrections.  Called by all threads
+// of a CTA.  `meta` selects the writer of the per-model words.
+__device__ void finalize_model(const KStack& st, int k, bool all_finite, bool meta, float* scratch,
+                               int scratch_floats) {
+  const int tid = threadIdx.x;
+  bool any_ok = false;
+  for (int r = tid; r < st.R; r += blockDim.x) any_ok |= st.ok[int64_t(k) * st.R + r] != 0;
+  const bool upd = __syncthreads_or(any_ok);
+  const bool active = upd && !st.frozen[k];
+  if (tid == 0 && active && !all_finite) atomicMin(&st.status[0], k);
+  if (!meta) return;
+  // stage the per-ray terms in smem (coalesced), then 3 threads sum them in
+  // numpy's pairwise order without a global-load latency per add
+  const float* terms = st.ray_terms + int64_t(k) * st.R * 3;
+  const bool staged = st.R * 3 <= scratch_floats;
+  if (staged) {
+    for (int i = tid; i < st.R * 3; i += blockDim.x) scratch[i] = __ldcg(terms + i);
+    __syncthreads();
+  }
+  if (tid < 3) {
+    const int j = tid;
+    const float sum = staged ? pairwise_sum([&](int64_t r) { return scratch[r * 3 + j]; }, st.R)
+                             : pairwise_sum([&](int64_t r) { return __ldcg(terms + r * 3 + j); }, st.R);
+    st.losses[int64_t(k) * 3 + j] = sum;
+    if (!isfinite(sum)) atomicMin(&st.status[1], k);
+  }
+  if (tid == 0) {
+    st.upd[k] = active ? 1 : 0;
+    const int64_t t = st.step[k] + 1;
+    float2 c;
+    if (t <= st.corr_len) {
+      c.x = st.corr1[t - 1];
+      c.y = st.corr2[t - 1];
+    } else {
+      c.x = 1.0f;
+      c.y = 1.0f;
+    }
+    st.corr[k] = c;
+  }
+}
+
+constexpr int kRedThreads = 128;
+constexpr int kRedLanes = 4;                                  // lanes per float4 of output
+constexpr int kRedChunk = kRedThreads / kRedLanes * 4;        // floats per reduce CTA
+
+// Sum the P partial gradient blocks of every split model in a fixed order
+// (deterministic): lane q of a 4-lane group adds partials
+// [q*P/4, (q+1)*P/4) sequentially, the four sub-sums are then added in lane
+// order.  One CTA per (model, 512-float chunk); chunk 0 also finalises.
+__global__ void __launch_bounds__(kRedThreads) reduce_partials_kernel(const __grid_constant__ KParams p) {
+  extern __shared__ __align__(16) float red_smem[];
+  int b = blockIdx.x, si = 0;
+  for (; si < p.n_stacks; ++si) {
+    const KStack& s = p.s[si];
+    if (s.P <= 1) continue;
+    const int n = s.K * ((s.block + kRedChunk - 1) / kRedChunk);
+    if (b < n) break;
+    b -= n;
+  }
+  if (si >= p.n_stacks) return;
+  const KStack& st = p.s[si];
+  const int chunks = (st.block + kRedChunk - 1) / kRedChunk;
+  const int k = b / chunks, ch = b % chunks;
+  const int q = threadIdx.x % kRedLanes;
+  const int i = ch * kRedChunk + 4 * (threadIdx.x / kRedLanes);
+  const int per = (st.P + kRedLanes - 1) / kRedLanes;
+  const int p0 = min(st.P, q * per), p1 = min(st.P, p0 + per);
+  float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (i < st.block && p0 < p1) {
+    const float* pb = st.partials + int64_t(k) * st.P * st.block + i;
+    const int64_t stride = st.block;
+    v = __ldcg(reinterpret_cast<const float4*>(pb + p0 * stride));
+    int pp = p0 + 1;
+    for (; pp + 8 <= p1; pp += 8) {  // 8 loads in flight, adds stay in order
+      float4 w[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) w[u] = __ldcg(reinterpret_cast<const float4*>(pb + (pp + u) * stride));
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        v.x += w[u].x; v.y += w[u].y; v.z += w[u].z; v.w += w[u].w;
+      }
+    }
+    for (; pp < p1; ++pp) {
+      const float4 w = __ldcg(reinterpret_cast<const float4*>(pb + pp * stride));
+      v.x += w.x; v.y += w.y; v.z += w.z; v.w += w.w;
+    }
+  }
+  // combine the 4 lanes' sub-sums in lane order (lane 0 ends with the total)
+  float4 tot = v;
+#pragma unroll
+  for (int l = 1; l < kRedLanes; ++l) {
+    const float x = __shfl_down_sync(0xffffffffu, v.x, l), y = __shfl_down_sync(0xffffffffu, v.y, l);
+    const float z = __shfl_down_sync(0xffffffffu, v.z, l), w = __shfl_down_sync(0xffffffffu, v.w, l);
+    if (q + l < kRedLanes) {
+      tot.x += x; tot.y += y; tot.z += z; tot.w += w;
+    }
+  }
+  bool finite = true;
+  if (q == 0 && i < st.block) {
+    st4(st.grads + int64_t(k) * st.block + i, tot);
+    finite = isfinite(tot.x) && isfinite(tot.y) && isfinite(tot.z) && isfinite(tot.w);
+  }
+  const bool all_finite = __syncthreads_and(finite);
+  finalize_model(st, k, all_finite, ch == 0, red_smem, st.R * 3);
+}
+
 template <int H, int L, int MODE>
 __device__ void run_item(const KStack& st, int item, float* smem) {
   using Cfg = TeamCfg<H>;
@@ -300,70 +410,21 @@ __device__ void run_item(const KStack& st, int item, float* smem) {
     for (int i = tid; i < st.block / 4; i += kThreads) st4(gdst + 4 * i, ld4(sW + 4 * i));
   }
 
-  // ---------------- per-model finalisation (last CTA of the model) ---------
-  __shared__ int s_last;
-  __threadfence();
+  // ---------------- per-model finalisation ---------
+  // Split models (P > 1) are reduced and finalised by reduce_partials_kernel;
+  // a single-CTA model finishes here.
+  if (st.P > 1) return;
   __syncthreads();
-  if (tid == 0) {
-    int last = 1;
-    if (st.P > 1) {
-      const int prev = atomicAdd(&st.counters[k], 1);
-      last = prev == st.P - 1;
-    }
-    s_last = last;
-  }
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-
-  float* gk = st.grads + int64_t(k) * st.block;
+  const float* gk = st.grads + int64_t(k) * st.block;
   bool finite = true;
   for (int i = tid; i < st.block / 4; i += kThreads) {
-    float4 v;
-    if (st.P > 1) {
-      const float* pbase = st.partials + int64_t(k) * st.P * st.block + 4 * i;
-      v = __ldcg(reinterpret_cast<const float4*>(pbase));
-      for (int p = 1; p < st.P; ++p) {
-        const float4 w = __ldcg(reinterpret_cast<const float4*>(pbase + int64_t(p) * st.block));
-        v.x += w.x; v.y += w.y; v.z += w.z; v.w += w.w;
-      }
-      st4(gk + 4 * i, v);
-    } else {
-      v = ld4(gk + 4 * i);
-    }
+    const float4 v = ld4(gk + 4 * i);
     finite &= isfinite(v.x) && isfinite(v.y) && isfinite(v.z) && isfinite(v.w);
   }
   const bool all_finite = __syncthreads_and(finite);
-
   if (MODE == kBackward) return;
-
-  // update mask = ray_ok.any(-1) (trainer.py:504)
-  bool any_ok = false;
-  for (int r = tid; r < st.R; r += kThreads) any_ok |= st.ok[int64_t(k) * st.R + r] != 0;
-  const bool upd = __syncthreads_or(any_ok);
-  if (tid < 3) {
-    const float* terms = st.ray_terms + int64_t(k) * st.R * 3;
-    const int j = tid;
-    const float sum = pairwise_sum([&](int64_t r) { return __ldcg(terms + r * 3 + j); }, st.R);
-    st.losses[int64_t(k) * 3 + j] = sum;
-    if (!isfinite(sum)) atomicMin(&st.status[1], k);
-  }
-  if (tid == 0) {
-    const bool active = upd && !st.frozen[k];
-    st.upd[k] = active ? 1 : 0;
-    if (active && !all_finite) atomicMin(&st.status[0], k);
-    const int64_t t = st.step[k] + 1;
-    float2 c;
-    if (t <= st.corr_len) {
-      c.x = st.corr1[t - 1];
-      c.y = st.corr2[t - 1];
-    } else {
-      c.x = 1.0f;
-      c.y = 1.0f;
-    }
-    st.corr[k] = c;
-    if (st.P > 1) st.counters[k] = 0;
-  }
+  // the team activation buffers are free now: stage per-ray terms there
+  finalize_model(st, k, all_finite, true, smem + st.w_floats, NTEAMS * st.team_floats);
 }
 
 template <int H0, int L0, int H1, int L1, int MODE>
@@ -488,16 +549,33 @@ static int launch_mlp(KernelFn fn, const KParams& p, int grid, size_t smem, cuda
 // a 120-ray hidden-32 object is one CTA, the 1200-ray hidden-128 background
 // about a hundred.
 constexpr double kTargetFlop = 24.0e6;
+constexpr int kSMs = 148;
+
+static int blocks_per_split(int nblk, int p) {
+  p = std::max(1, std::min(p, nblk));
+  return (nblk + p - 1) / p;
+}
 
 static int choose_splits(const KStack* ks, int n, int* P) {
+  int nblk[2], total = 0;
   for (int i = 0; i < n; ++i) {
     const double flop_per_sample = double(ks[i].H) * (ks[i].Dp + 2 * (ks[i].L - 2) * ks[i].H + 8) * 3.0;
     const double cost = flop_per_sample * ks[i].R * ks[i].S;
-    const int nblk = (ks[i].R + ks[i].G - 1) / ks[i].G;
-    int p = int(cost / kTargetFlop + 0.5);
-    p = std::max(1, std::min(p, nblk));
-    const int bps = (nblk + p - 1) / p;  // blocks per CTA; drop empty CTAs
-    P[i] = (nblk + bps - 1) / bps;
+    nblk[i] = (ks[i].R + ks[i].G - 1) / ks[i].G;
+    const int bps = blocks_per_split(nblk[i], int(cost / kTargetFlop + 0.5));
+    P[i] = (nblk[i] + bps - 1) / bps;  // drop empty CTAs
+    total += ks[i].K * P[i];
+  }
+  // Keep a multi-stack launch within one wave of 148 SMs: a second wave of a
+  // few CTAs doubles the kernel time.  Shrink the most-split stack to fit.
+  if (n > 1 && total > kSMs) {
+    int big = ks[0].K * P[0] >= ks[1].K * P[1] ? 0 : 1;
+    const int others = total - ks[big].K * P[big];
+    const int budget = (kSMs - others) / std::max(1, ks[big].K);
+    if (budget >= 1 && P[big] > 1) {
+      const int bps = blocks_per_split(nblk[big], budget);
+      P[big] = (nblk[big] + bps - 1) / bps;
+    }
   }
   return VM_OK;
 }
@@ -511,6 +589,7 @@ namespace {
 // it to report the kernel's roofline fraction from the timed region itself).
 struct KernelProfiler {
   bool on = false;
+  long kernels = 0;  // every kernel launched by vm_train_step / vm_sample while on
   std::vector<cudaEvent_t> ev;  // start/stop pairs
   size_t used = 0;
   cudaEvent_t get() {
@@ -623,8 +702,6 @@ extern "C" int vm_train_step(const VmStack* stacks, const VmBatch* batches, int 
   cudaStream_t s = cudaStream_t(stream);
   char* ws = static_cast<char*>(workspace);
   VM_CUDA(cudaMemsetAsync(status, 0x7f, sizeof(int32_t) * 4 * n_stacks, s));
-  for (int i = 0; i < n_stacks; ++i)  // last-CTA tickets (the workspace may have held another plan)
-    if (pl.kp.s[i].P > 1) VM_CUDA(cudaMemsetAsync(ws + pl.off_cnt[i], 0, size_t(pl.kp.s[i].K) * 4, s));
   int loss_off = 0;
   for (int i = 0; i < n_stacks; ++i) {
     KStack& ks = pl.kp.s[i];
@@ -665,10 +742,25 @@ extern "C" int vm_train_step(const VmStack* stacks, const VmBatch* batches, int 
   }
   rc = launch_mlp(fn, pl.kp, pl.grid, pl.smem, s);
   if (rc) return rc;
+  if (g_prof.on) g_prof.kernels += 1;
   if (g_prof.on) VM_CUDA(cudaEventRecord(e1, s));
+  int red_grid = 0;
+  for (int i = 0; i < n_stacks; ++i)
+    if (pl.kp.s[i].P > 1) red_grid += pl.kp.s[i].K * ((pl.kp.s[i].block + kRedChunk - 1) / kRedChunk);
+  if (red_grid > 0) {
+    int red_smem = 0;
+    for (int i = 0; i < n_stacks; ++i)
+      if (pl.kp.s[i].P > 1) red_smem = std::max(red_smem, pl.kp.s[i].R * 3 * 4);
+    if (red_smem > 48 * 1024)
+      VM_CUDA(cudaFuncSetAttribute(reduce_partials_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, red_smem));
+    reduce_partials_kernel<<<red_grid, kRedThreads, red_smem, s>>>(pl.kp);
+    VM_CUDA(cudaGetLastError());
+    if (g_prof.on) g_prof.kernels += 1;
+  }
   if (pl.adam_grid > 0) {
     adam_train_kernel<<<pl.adam_grid, 256, 0, s>>>(pl.ap);
     VM_CUDA(cudaGetLastError());
+    if (g_prof.on) g_prof.kernels += 1;
   }
   return VM_OK;
 }
@@ -730,6 +822,16 @@ extern "C" int vm_backward(const VmStack* st, const float* encoded, int64_t n_sa
 extern "C" int vm_profile_enable(int on) {
   g_prof.on = on != 0;
   g_prof.used = 0;
+  g_prof.kernels = 0;
+  return VM_OK;
+}
+
+extern "C" void vm_profile_count_kernels(int n) {
+  if (g_prof.on) g_prof.kernels += n;
+}
+
+extern "C" int vm_profile_kernels(long* n) {
+  *n = g_prof.kernels;
   return VM_OK;
 }
 

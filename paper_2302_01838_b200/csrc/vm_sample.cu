@@ -58,10 +58,25 @@ __device__ u128 pcg_advance(u128 state, u128 inc, uint64_t delta) {
   return acc_mult * state + acc_plus;
 }
 
+// Jump tables: advancing by 2^k steps is s -> A[k]*s + G[k]*inc with
+// A[k] = M^(2^k), G[k] = sum_{i<2^k} M^i (mod 2^128); filled once on the host.
+constexpr int kJumpBits = 48;
+__constant__ u128 c_jumpA[kJumpBits];
+__constant__ u128 c_jumpG[kJumpBits];
+
+__device__ __forceinline__ u128 pcg_jump(u128 s, u128 inc, uint64_t delta) {
+#pragma unroll 1
+  for (int k = 0; k < kJumpBits; ++k) {
+    if (!__any_sync(__activemask(), (delta >> k) != 0)) break;  // warp-uniform exit
+    if ((delta >> k) & 1) s = c_jumpA[k] * s + c_jumpG[k] * inc;
+  }
+  return s;
+}
+
 struct Stream {
   u128 state0, inc;
   // Cursor positioned so that next() returns word `pos`.
-  __device__ __forceinline__ u128 at(uint64_t pos) const { return pcg_advance(state0, inc, pos); }
+  __device__ __forceinline__ u128 at(uint64_t pos) const { return pcg_jump(state0, inc, pos); }
 };
 
 __device__ __forceinline__ uint64_t next_word(u128& s, u128 inc) {
@@ -202,7 +217,11 @@ struct KS {
   uint8_t* ok;
   float* points;    // [K,R,S,3] f32 (encode == 0)
   double* p64;      // [K,R,S,3] f64 workspace (encode == 1)
-  double* nrm;      // [K,N] resolved normals (workspace)
+  // workspace written by the per-object prep kernel
+  Stream* streams;  // [K][2] PIXELS, SAMPLES
+  int* kf;          // [K,R] keyframe index per ray
+  int64_t* bases;   // [K][2] first uv word (PIXELS), first u_fallback word (SAMPLES)
+  double* nrm;      // [K,N] resolved normals
   int* status;      // [K] fallback flags (diagnostics)
   int64_t* aux_kf;
   int64_t* aux_u;
@@ -237,85 +256,74 @@ __device__ int block_exclusive_scan(int v, int* scratch, int& total) {
 }
 
 constexpr int kST = 256;
+constexpr int kRT = 128;  // per-ray kernel block size
 
-__global__ void __launch_bounds__(kST) sample_kernel(const __grid_constant__ KS ks) {
+__device__ __forceinline__ bool object_live(const VmSampleObject& ob) { return ob.active && ob.n_kf > 0; }
+
+// ---- per object: stream seeds, keyframe index per ray, normal resolution.
+__global__ void __launch_bounds__(kST) sample_prep_kernel(const __grid_constant__ KS ks) {
   extern __shared__ __align__(16) unsigned char sm[];
   __shared__ uint64_t s_ki[256];
   __shared__ double s_wi[256], s_fi[256];
   __shared__ Stream s_pix, s_smp;
-  __shared__ int s_scan[16], s_flag, s_kfwords, s_nseg, s_nov, s_end;
+  __shared__ int s_scan[16], s_flag, s_nseg, s_nov, s_end;
+  __shared__ int64_t s_kfwords;
 
   const int k = blockIdx.x, tid = threadIdx.x;
   const VmSampleObject ob = ks.objs[k];
+  if (!object_live(ob)) return;
   const VmSampleParams& P = ks.p;
-  const int R = P.n_rays, S = ks.S, nc = P.n_stratified, nsf = P.n_surface, N = ks.N, W = ks.W;
-  const int64_t rbase = int64_t(k) * R;
+  const int R = P.n_rays, nc = P.n_stratified, N = ks.N, W = ks.W;
 
-  if (!ob.active || ob.n_kf <= 0) {  // zero batch (trainer.py:190-200, :272-273)
-    for (int i = tid; i < R * S; i += kST) {
-      ks.t32[rbase * S + i] = 0.f;
-      if (ks.points) {
-        for (int c = 0; c < 3; ++c) ks.points[(rbase * S + i) * 3 + c] = 0.f;
-      }
-      if (ks.p64) {
-        for (int c = 0; c < 3; ++c) ks.p64[(rbase * S + i) * 3 + c] = 0.0;
-      }
-      if (ks.aux_t64) ks.aux_t64[rbase * S + i] = 0.0;
-    }
-    for (int r = tid; r < R; r += kST) {
-      ks.tdepth[rbase + r] = 0.f;
-      for (int c = 0; c < 3; ++c) ks.tcol[(rbase + r) * 3 + c] = 0.f;
-      ks.tmask[rbase + r] = 0;
-      ks.valid[rbase + r] = 0;
-      ks.ok[rbase + r] = 0;
-      if (ks.aux_kf) {
-        ks.aux_kf[rbase + r] = 0;
-        ks.aux_u[rbase + r] = 0;
-        ks.aux_v[rbase + r] = 0;
-      }
-    }
-    return;
-  }
-
-  // smem carve-up
   double* xs = reinterpret_cast<double*>(sm);                  // [W]
   double* ov_val = xs + W;                                     // [SC]
   int* slow = reinterpret_cast<int*>(ov_val + ks.SC);          // [SC]
   int* seg_j = slow + ks.SC;                                   // [SC+1]
   int* seg_off = seg_j + ks.SC + 1;                            // [SC+1]
   int* ov_j = seg_off + ks.SC + 1;                             // [SC]
-  int* kf_s = ov_j + ks.SC;                                    // [R]
-  uint8_t* fastf = reinterpret_cast<uint8_t*>(kf_s + R);       // [W]
+  uint8_t* fastf = reinterpret_cast<uint8_t*>(ov_j + ks.SC);   // [W]
 
   for (int i = tid; i < 256; i += kST) {
     s_ki[i] = vm_zig_ki[i];
     s_wi[i] = __longlong_as_double(static_cast<long long>(vm_zig_wi[i]));
     s_fi[i] = __longlong_as_double(static_cast<long long>(vm_zig_fi[i]));
   }
-  if (tid == 0) s_pix = seed_stream(P.seed, 3, uint64_t(ob.object_id), uint64_t(P.step));
-  if (tid == 32) s_smp = seed_stream(P.seed, 4, uint64_t(ob.object_id), uint64_t(P.step));
+  const uint64_t step = P.step_dev ? uint64_t(*P.step_dev + P.step_offset) : uint64_t(P.step);
+  if (tid == 0) s_pix = seed_stream(P.seed, 3, uint64_t(ob.object_id), step);
+  if (tid == 32) s_smp = seed_stream(P.seed, 4, uint64_t(ob.object_id), step);
   if (tid == 64) s_flag = 0;
   __syncthreads();
   const Zig zig{s_ki, s_wi, s_fi};
   const Stream pix = s_pix, smp = s_smp;
+  if (tid == 0) {
+    ks.streams[2 * k] = pix;
+    ks.streams[2 * k + 1] = smp;
+  }
 
   // ---------------- keyframe index per ray (objects.py:336) ----------------
+  int* kf_out = ks.kf + int64_t(k) * R;
   const int n_kf = ob.n_kf;
   if (n_kf == 1) {
-    for (int r = tid; r < R; r += kST) kf_s[r] = 0;
+    for (int r = tid; r < R; r += kST) kf_out[r] = 0;
     if (tid == 0) s_kfwords = 0;
   } else {
     const uint32_t n = uint32_t(n_kf);
     const uint32_t thr = uint32_t((uint64_t(1) << 32) - n) % n;
     bool rej = false;
-    for (int r = tid; r < R; r += kST) {
-      u128 s = pix.at(uint64_t(r >> 1));
-      const uint64_t w = next_word(s, pix.inc);
-      const uint32_t x = (r & 1) ? uint32_t(w >> 32) : uint32_t(w);
-      const uint64_t m = uint64_t(x) * n;
-      const uint32_t left = uint32_t(m);
-      if (left < n && left < thr) rej = true;
-      kf_s[r] = int(m >> 32);
+    // two rays (low/high half) per 64-bit word; consecutive words per thread
+    for (int w = tid; w < (R + 1) / 2; w += kST) {
+      u128 s = pix.at(uint64_t(w));
+      const uint64_t word = next_word(s, pix.inc);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int r = 2 * w + h;
+        if (r >= R) break;
+        const uint32_t x = h ? uint32_t(word >> 32) : uint32_t(word);
+        const uint64_t m = uint64_t(x) * n;
+        const uint32_t left = uint32_t(m);
+        if (left < n && left < thr) rej = true;
+        kf_out[r] = int(m >> 32);
+      }
     }
     if (__syncthreads_or(rej)) {
       if (tid == 0) {  // rare: replay the buffered Lemire draws sequentially
@@ -336,9 +344,9 @@ __global__ void __launch_bounds__(kST) sample_kernel(const __grid_constant__ KS 
           const uint64_t m = uint64_t(x) * n;
           const uint32_t left = uint32_t(m);
           if (left < n && left < thr) continue;
-          kf_s[r++] = int(m >> 32);
+          kf_out[r++] = int(m >> 32);
         }
-        s_kfwords = int(words);
+        s_kfwords = int64_t(words);
         s_flag |= 1;
       }
     } else if (tid == 0) {
@@ -346,9 +354,9 @@ __global__ void __launch_bounds__(kST) sample_kernel(const __grid_constant__ KS 
     }
   }
 
-  // ---------------- normals window (render.py:185) ----------------
-  // classify window positions [0, W) of the normals region
+  // ---------------- normals (render.py:185) ----------------
   const uint64_t nbase = uint64_t(nc) * R;
+  int total = 0;
   {
     const int per = (W + kST - 1) / kST;
     const int p0 = tid * per, p1 = min(W, p0 + per);
@@ -362,7 +370,6 @@ __global__ void __launch_bounds__(kST) sample_kernel(const __grid_constant__ KS 
         cnt += !f;
       }
     }
-    int total;
     int off = block_exclusive_scan(cnt, s_scan, total);
     if (total > ks.SC) {
       if (tid == 0) s_flag |= 2;
@@ -371,23 +378,21 @@ __global__ void __launch_bounds__(kST) sample_kernel(const __grid_constant__ KS 
         if (!fastf[p]) slow[off++] = p;
     }
     __syncthreads();
-    // speculative slow-path resolution, one thread per slow position
-    if (!(s_flag & 2)) {
+    if (!(s_flag & 2)) {  // speculative slow-path resolution, one thread per slow position
       for (int i = tid; i < total; i += kST) {
         double v;
         bool acc;
         const int used = zig_slow(smp, nbase + slow[i], zig, v, acc);
         ov_val[i] = v;
-        seg_off[i] = acc ? used : -used;  // temporarily: +consumed (accepted) / -consumed (rejected)
+        ov_j[i] = acc ? used : -used;  // +consumed (accepted) / -consumed (rejected)
       }
     }
     __syncthreads();
     if (tid == 0 && !(s_flag & 2)) {
-      // walk the slow list; seg_j/seg_off become segment starts/offsets,
-      // ov_j/ov_val the accepted slow normals (compacted in place).
+      // walk the slow list: seg_j/seg_off = segment starts/offsets of fast
+      // normals; slow[]/ov_val[] are compacted in place to the accepted slow
+      // normals (index, value).
       int pos = 0, j = 0, nseg = 1, nov = 0;
-      int* res = seg_off;  // read results before overwriting: keep a copy in ov_j scratch
-      for (int i = 0; i < total; ++i) ov_j[i] = res[i];
       seg_j[0] = 0;
       seg_off[0] = 0;
       for (int i = 0; i < total && j < N; ++i) {
@@ -398,7 +403,7 @@ __global__ void __launch_bounds__(kST) sample_kernel(const __grid_constant__ KS 
         const int r = ov_j[i];
         if (r > 0) {
           ov_val[nov] = ov_val[i];
-          slow[nov] = j;  // reuse slow[] for the override normal index (i >= nov)
+          slow[nov] = j;
           ++nov;
           ++j;
           pos = s + r;
@@ -419,8 +424,7 @@ __global__ void __launch_bounds__(kST) sample_kernel(const __grid_constant__ KS 
   }
   double* nrm = ks.nrm + int64_t(k) * N;
   if (s_flag & 2) {
-    // window overflow (practically unreachable): sequential ziggurat replay
-    if (tid == 0) {
+    if (tid == 0) {  // window overflow (practically unreachable): sequential replay
       u128 s = smp.at(nbase);
       uint64_t used = 0;
       for (int j = 0; j < N; ++j) {
@@ -444,7 +448,6 @@ __global__ void __launch_bounds__(kST) sample_kernel(const __grid_constant__ KS 
         }
       }
       s_end = int(used);
-      ks.status[k] = s_flag;
     }
   } else {
     const int nseg = s_nseg, nov = s_nov;
@@ -455,145 +458,179 @@ __global__ void __launch_bounds__(kST) sample_kernel(const __grid_constant__ KS 
         if (seg_j[mid] <= j) lo = mid;
         else hi = mid - 1;
       }
-      int a = 0, b = nov - 1, hit = -1;  // override lookup
+      int a = 0, b = nov - 1, hit = -1;  // accepted-slow override
       while (a <= b) {
         const int mid = (a + b) >> 1;
-        if (slow[mid] == j) { hit = mid; break; }
+        if (slow[mid] == j) {
+          hit = mid;
+          break;
+        }
         if (slow[mid] < j) a = mid + 1;
         else b = mid - 1;
       }
       nrm[j] = hit >= 0 ? ov_val[hit] : xs[j + seg_off[lo]];
     }
-    if (tid == 0) ks.status[k] = s_flag;
   }
   __syncthreads();
-  const uint64_t fb_base = nbase + uint64_t(s_end);
-  const uint64_t uv_base = uint64_t(s_kfwords);
+  if (tid == 0) {
+    ks.bases[2 * k] = s_kfwords;
+    ks.bases[2 * k + 1] = int64_t(nbase) + s_end;
+    ks.status[k] = s_flag;
+  }
+}
 
-  // ---------------- per ray ----------------
-  for (int r = tid; r < R; r += kST) {
-    const int kfi = kf_s[r];
-    const VmKeyframe& kf = ks.kfs[ob.kf_begin + kfi];
-    u128 s = pix.at(uv_base + 2 * uint64_t(r));
-    const double du = word_to_double(next_word(s, pix.inc));
-    const double dv = word_to_double(next_word(s, pix.inc));
-    int64_t u = kf.u0 + int64_t(floor(du * double(kf.u1 - kf.u0)));
-    int64_t v = kf.v0 + int64_t(floor(dv * double(kf.v1 - kf.v0)));
-    u = u < int64_t(kf.u1 - 1) ? u : int64_t(kf.u1 - 1);
-    v = v < int64_t(kf.v1 - 1) ? v : int64_t(kf.v1 - 1);
-    const int64_t tix = kf.texel_off + (v - kf.v0) * (kf.u1 - kf.u0) + (u - kf.u0);
-    const float4 px = ks.rgbd[tix];
-    const bool in_mask = ks.mask[tix] != 0;
-
-    // rays (trainer.py:289-297): camera dirs, rotate, normalise
-    const double d0 = (double(u) - P.cx) / P.fx;
-    const double d1 = (double(v) - P.cy) / P.fy;
-    const double to_t = sqrt((d0 * d0 + d1 * d1) + 1.0);
-    double dir[3], org[3];
-#pragma unroll
-    for (int i = 0; i < 3; ++i) {
-      // einsum "rij,rj->ri": (R[i][0]*d0 + R[i][2]*1.0) + R[i][1]*d1
-      dir[i] = (kf.pose[4 * i + 0] * d0 + kf.pose[4 * i + 2] * 1.0) + kf.pose[4 * i + 1] * d1;
-      org[i] = kf.pose[4 * i + 3];
-    }
-    const double dn = sqrt((dir[0] * dir[0] + dir[1] * dir[1]) + dir[2] * dir[2]);
-#pragma unroll
-    for (int i = 0; i < 3; ++i) dir[i] = dir[i] / dn;
-    const double z = double(px.w);
-    const bool valid = z > 0.0;
-    const double surf = z * to_t;
-
-    // ray_box_intersect (render.py:111-139) on the padded box
-    double tin = -INFINITY, tout = INFINITY;
-#pragma unroll
-    for (int i = 0; i < 3; ++i) {
-      double lo, hi;
-      if (dir[i] == 0.0) {
-        const bool inside = (org[i] >= ob.box_min[i]) && (org[i] <= ob.box_max[i]);
-        lo = inside ? -INFINITY : INFINITY;
-        hi = inside ? INFINITY : -INFINITY;
-      } else {
-        const double inv = 1.0 / dir[i];
-        const double ta = (ob.box_min[i] - org[i]) * inv;
-        const double tb = (ob.box_max[i] - org[i]) * inv;
-        lo = np_min_d(ta, tb);
-        hi = np_max_d(ta, tb);
-      }
-      tin = i == 0 ? lo : np_max_d(tin, lo);
-      tout = i == 0 ? hi : np_min_d(tout, hi);
-    }
-    const double t_entry = np_max_d(tin, 0.0);
-    const bool hit = (tout >= t_entry) && (tout >= 0.0);
-    const double near_ = hit ? np_max_d(t_entry, P.t_near) : P.t_near;
-    const double far_ = (hit && tout > near_) ? tout : P.t_far;
-
-    // sample_along_rays (render.py:149-227)
-    const double lo = near_;
-    const double far2 = np_max_d(far_, lo);
-    const bool has_depth = valid && (surf > lo);
-    const bool near_block = valid && !has_depth;
-    const bool over = in_mask && has_depth && (surf > far2 + P.three_std);
-    const bool guided = in_mask && has_depth && !over;
-    const double upper = in_mask ? far2 : (has_depth ? np_min_d(surf, far2) : far2);
-    const bool ray_ok = (guided || upper > lo) && !near_block && !over;
-    double t[32];
-    if (guided) {
-      u128 q = smp.at(uint64_t(nc) * r);
-      for (int i = 0; i < nc; ++i) {
-        const double us = word_to_double(next_word(q, smp.inc));
-        t[i] = lo + ((double(i) + us) / double(nc)) * (surf - lo);
-      }
-      const double band_hi = np_min_d(surf + P.three_std, far2);
-      for (int i = 0; i < nsf; ++i) {
-        const double a = surf + P.surface_std * nrm[int64_t(r) * nsf + i];
-        t[nc + i] = np_min_d(np_max_d(a, lo), band_hi);
-      }
-    } else {
-      u128 q = smp.at(fb_base + uint64_t(S) * r);
-      const double hi_f = np_max_d(upper, lo);
-      for (int i = 0; i < S; ++i) {
-        const double uf = word_to_double(next_word(q, smp.inc));
-        t[i] = lo + ((double(i) + uf) / double(S)) * (hi_f - lo);
-      }
-    }
-    for (int i = 1; i < S; ++i) {  // ascending insertion sort
-      const double x = t[i];
-      int j = i - 1;
-      while (j >= 0 && t[j] > x) {
-        t[j + 1] = t[j];
-        --j;
-      }
-      t[j + 1] = x;
-    }
-
-    const int64_t rg = rbase + r;
-    ks.tdepth[rg] = float(surf);
-    ks.tcol[rg * 3 + 0] = px.x;
-    ks.tcol[rg * 3 + 1] = px.y;
-    ks.tcol[rg * 3 + 2] = px.z;
-    ks.tmask[rg] = in_mask;
-    ks.valid[rg] = valid;
-    ks.ok[rg] = ray_ok;
-    if (ks.aux_kf) {
-      ks.aux_kf[rg] = kfi;
-      ks.aux_u[rg] = u;
-      ks.aux_v[rg] = v;
-    }
+// ---- per ray: pixel, gathers, f64 geometry, depth-guided samples, outputs.
+__global__ void __launch_bounds__(kRT) sample_rays_kernel(const __grid_constant__ KS ks, int n_objects) {
+  const VmSampleParams& P = ks.p;
+  const int R = P.n_rays, S = ks.S, nc = P.n_stratified, nsf = P.n_surface;
+  const int64_t rg = blockIdx.x * int64_t(kRT) + threadIdx.x;
+  if (rg >= int64_t(n_objects) * R) return;
+  const int k = int(rg / R), r = int(rg % R);
+  const VmSampleObject& ob = ks.objs[k];
+  if (!object_live(ob)) {  // zero batch (trainer.py:190-200, :272-273)
     for (int i = 0; i < S; ++i) {
-      const int64_t sg = rg * S + i;
-      ks.t32[sg] = float(t[i]);
-      if (ks.aux_t64) ks.aux_t64[sg] = t[i];
-      double pn[3];
+      ks.t32[rg * S + i] = 0.f;
+      if (ks.points)
+        for (int c = 0; c < 3; ++c) ks.points[(rg * S + i) * 3 + c] = 0.f;
+      if (ks.p64)
+        for (int c = 0; c < 3; ++c) ks.p64[(rg * S + i) * 3 + c] = 0.0;
+      if (ks.aux_t64) ks.aux_t64[rg * S + i] = 0.0;
+    }
+    ks.tdepth[rg] = 0.f;
+    for (int c = 0; c < 3; ++c) ks.tcol[rg * 3 + c] = 0.f;
+    ks.tmask[rg] = 0;
+    ks.valid[rg] = 0;
+    ks.ok[rg] = 0;
+    if (ks.aux_kf) {
+      ks.aux_kf[rg] = 0;
+      ks.aux_u[rg] = 0;
+      ks.aux_v[rg] = 0;
+    }
+    return;
+  }
+  const Stream pix = ks.streams[2 * k], smp = ks.streams[2 * k + 1];
+  const uint64_t uv_base = uint64_t(ks.bases[2 * k]), fb_base = uint64_t(ks.bases[2 * k + 1]);
+  const int kfi = ks.kf[rg];
+  const VmKeyframe& kf = ks.kfs[ob.kf_begin + kfi];
+  u128 s = pix.at(uv_base + 2 * uint64_t(r));
+  const double du = word_to_double(next_word(s, pix.inc));
+  const double dv = word_to_double(next_word(s, pix.inc));
+  int64_t u = kf.u0 + int64_t(floor(du * double(kf.u1 - kf.u0)));
+  int64_t v = kf.v0 + int64_t(floor(dv * double(kf.v1 - kf.v0)));
+  u = u < int64_t(kf.u1 - 1) ? u : int64_t(kf.u1 - 1);
+  v = v < int64_t(kf.v1 - 1) ? v : int64_t(kf.v1 - 1);
+  const int64_t tix = kf.texel_off + (v - kf.v0) * (kf.u1 - kf.u0) + (u - kf.u0);
+  const float4 px = ks.rgbd[tix];
+  const bool in_mask = ks.mask[tix] != 0;
+
+  // rays (trainer.py:289-297): camera dirs, rotate, normalise
+  const double d0 = (double(u) - P.cx) / P.fx;
+  const double d1 = (double(v) - P.cy) / P.fy;
+  const double to_t = sqrt((d0 * d0 + d1 * d1) + 1.0);
+  double dir[3], org[3];
 #pragma unroll
-      for (int c = 0; c < 3; ++c) pn[c] = ((org[c] + t[i] * dir[c]) - ob.center[c]) / ob.half[c];
-      if (ks.points) {
+  for (int i = 0; i < 3; ++i) {
+    // einsum "rij,rj->ri": (R[i][0]*d0 + R[i][2]*1.0) + R[i][1]*d1
+    dir[i] = (kf.pose[4 * i + 0] * d0 + kf.pose[4 * i + 2] * 1.0) + kf.pose[4 * i + 1] * d1;
+    org[i] = kf.pose[4 * i + 3];
+  }
+  const double dn = sqrt((dir[0] * dir[0] + dir[1] * dir[1]) + dir[2] * dir[2]);
 #pragma unroll
-        for (int c = 0; c < 3; ++c) ks.points[sg * 3 + c] = float(pn[c]);
-      }
-      if (ks.p64) {
+  for (int i = 0; i < 3; ++i) dir[i] = dir[i] / dn;
+  const double z = double(px.w);
+  const bool valid = z > 0.0;
+  const double surf = z * to_t;
+
+  // ray_box_intersect (render.py:111-139) on the padded box
+  double tin = -INFINITY, tout = INFINITY;
 #pragma unroll
-        for (int c = 0; c < 3; ++c) ks.p64[sg * 3 + c] = pn[c];
-      }
+  for (int i = 0; i < 3; ++i) {
+    double lo, hi;
+    if (dir[i] == 0.0) {
+      const bool inside = (org[i] >= ob.box_min[i]) && (org[i] <= ob.box_max[i]);
+      lo = inside ? -INFINITY : INFINITY;
+      hi = inside ? INFINITY : -INFINITY;
+    } else {
+      const double inv = 1.0 / dir[i];
+      const double ta = (ob.box_min[i] - org[i]) * inv;
+      const double tb = (ob.box_max[i] - org[i]) * inv;
+      lo = np_min_d(ta, tb);
+      hi = np_max_d(ta, tb);
+    }
+    tin = i == 0 ? lo : np_max_d(tin, lo);
+    tout = i == 0 ? hi : np_min_d(tout, hi);
+  }
+  const double t_entry = np_max_d(tin, 0.0);
+  const bool hit = (tout >= t_entry) && (tout >= 0.0);
+  const double near_ = hit ? np_max_d(t_entry, P.t_near) : P.t_near;
+  const double far_ = (hit && tout > near_) ? tout : P.t_far;
+
+  // sample_along_rays (render.py:149-227)
+  const double lo = near_;
+  const double far2 = np_max_d(far_, lo);
+  const bool has_depth = valid && (surf > lo);
+  const bool near_block = valid && !has_depth;
+  const bool over = in_mask && has_depth && (surf > far2 + P.three_std);
+  const bool guided = in_mask && has_depth && !over;
+  const double upper = in_mask ? far2 : (has_depth ? np_min_d(surf, far2) : far2);
+  const bool ray_ok = (guided || upper > lo) && !near_block && !over;
+  double t[32];
+  if (guided) {
+    u128 q = smp.at(uint64_t(nc) * r);
+    for (int i = 0; i < nc; ++i) {
+      const double us = word_to_double(next_word(q, smp.inc));
+      t[i] = lo + ((double(i) + us) / double(nc)) * (surf - lo);
+    }
+    const double band_hi = np_min_d(surf + P.three_std, far2);
+    const double* nz = ks.nrm + int64_t(k) * ks.N + int64_t(r) * nsf;
+    for (int i = 0; i < nsf; ++i) {
+      const double a = surf + P.surface_std * nz[i];
+      t[nc + i] = np_min_d(np_max_d(a, lo), band_hi);
+    }
+  } else {
+    u128 q = smp.at(fb_base + uint64_t(S) * r);
+    const double hi_f = np_max_d(upper, lo);
+    for (int i = 0; i < S; ++i) {
+      const double uf = word_to_double(next_word(q, smp.inc));
+      t[i] = lo + ((double(i) + uf) / double(S)) * (hi_f - lo);
+    }
+  }
+  for (int i = 1; i < S; ++i) {  // ascending insertion sort
+    const double x = t[i];
+    int j = i - 1;
+    while (j >= 0 && t[j] > x) {
+      t[j + 1] = t[j];
+      --j;
+    }
+    t[j + 1] = x;
+  }
+
+  ks.tdepth[rg] = float(surf);
+  ks.tcol[rg * 3 + 0] = px.x;
+  ks.tcol[rg * 3 + 1] = px.y;
+  ks.tcol[rg * 3 + 2] = px.z;
+  ks.tmask[rg] = in_mask;
+  ks.valid[rg] = valid;
+  ks.ok[rg] = ray_ok;
+  if (ks.aux_kf) {
+    ks.aux_kf[rg] = kfi;
+    ks.aux_u[rg] = u;
+    ks.aux_v[rg] = v;
+  }
+  for (int i = 0; i < S; ++i) {
+    const int64_t sg = rg * S + i;
+    ks.t32[sg] = float(t[i]);
+    if (ks.aux_t64) ks.aux_t64[sg] = t[i];
+    double pn[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) pn[c] = ((org[c] + t[i] * dir[c]) - ob.center[c]) / ob.half[c];
+    if (ks.points) {
+#pragma unroll
+      for (int c = 0; c < 3; ++c) ks.points[sg * 3 + c] = float(pn[c]);
+    }
+    if (ks.p64) {
+#pragma unroll
+      for (int c = 0; c < 3; ++c) ks.p64[sg * 3 + c] = pn[c];
     }
   }
 }
@@ -632,7 +669,7 @@ __global__ void encode_kernel(int64_t n_samples, int n_freq, int include, int D,
 struct SamplePlan {
   int S, N, W, SC;
   size_t smem;
-  size_t off_nrm, off_status, off_p64, bytes;
+  size_t off_streams, off_kf, off_bases, off_nrm, off_status, off_p64, bytes;
 };
 
 SamplePlan plan_sample(int n_objects, const VmSampleParams& p) {
@@ -642,13 +679,16 @@ SamplePlan plan_sample(int n_objects, const VmSampleParams& p) {
   pl.W = pl.N + pl.N / 16 + 64;
   pl.SC = pl.W / 8 + 64;
   pl.smem = size_t(pl.W) * 8 + size_t(pl.SC) * 8 + size_t(pl.SC) * 4 * 2 + size_t(pl.SC + 1) * 4 * 2 +
-            size_t(p.n_rays) * 4 + size_t(pl.W) + 16;
+            size_t(pl.W) + 16;
   size_t off = 0;
   auto take = [&](size_t b) {
     const size_t o = off;
     off = (off + b + 255) / 256 * 256;
     return o;
   };
+  pl.off_streams = take(size_t(n_objects) * 2 * sizeof(Stream));
+  pl.off_kf = take(size_t(n_objects) * p.n_rays * 4);
+  pl.off_bases = take(size_t(n_objects) * 2 * 8);
   pl.off_nrm = take(size_t(n_objects) * pl.N * 8 + 8);
   pl.off_status = take(size_t(n_objects) * 4 + 4);
   pl.off_p64 = take(p.encode ? size_t(n_objects) * p.n_rays * pl.S * 3 * 8 : 0);
@@ -656,10 +696,41 @@ SamplePlan plan_sample(int n_objects, const VmSampleParams& p) {
   return pl;
 }
 
+// Host: jump tables A[k] = M^(2^k), G[k] = 1 + M + ... + M^(2^k - 1) (mod 2^128).
+int ensure_jump_tables() {
+  static bool ready = false;
+  if (ready) return VM_OK;
+  const u128 M = (u128(2549297995355413924ULL) << 64) | u128(4865540595714422341ULL);
+  u128 A[kJumpBits], G[kJumpBits];
+  u128 a = M, g = 1;
+  for (int k = 0; k < kJumpBits; ++k) {
+    A[k] = a;
+    G[k] = g;
+    g = g * (a + 1);  // sum_{i<2^(k+1)} M^i = (1 + M^(2^k)) * sum_{i<2^k} M^i
+    a = a * a;
+  }
+  VM_CUDA(cudaMemcpyToSymbol(c_jumpA, A, sizeof(A)));
+  VM_CUDA(cudaMemcpyToSymbol(c_jumpG, G, sizeof(G)));
+  ready = true;
+  return VM_OK;
+}
+
 }  // namespace
 }  // namespace vm
 
 using namespace vm;
+
+extern "C" void vm_profile_count_kernels(int n);
+
+namespace vm {
+__global__ void step_advance_kernel(int64_t* c, int64_t inc) { *c += inc; }
+}  // namespace vm
+
+extern "C" int vm_step_advance(int64_t* counter, int64_t inc, void* stream) {
+  step_advance_kernel<<<1, 1, 0, cudaStream_t(stream)>>>(counter, inc);
+  VM_CUDA(cudaGetLastError());
+  return VM_OK;
+}
 
 extern "C" size_t vm_sample_workspace_bytes(int n_objects, const VmSampleParams* params) {
   if (!params || n_objects < 0) return 0;
@@ -680,6 +751,8 @@ extern "C" int vm_sample(const VmSampleObject* objects, int n_objects, const VmK
   if (n_objects == 0) return VM_OK;
   if (p.encode) VM_REQUIRE(out->encoded != nullptr, "vm_sample: encoded output missing");
   else VM_REQUIRE(out->points != nullptr, "vm_sample: points output missing");
+  int rc = ensure_jump_tables();
+  if (rc) return rc;
   char* ws = static_cast<char*>(workspace);
   KS ks;
   std::memset(&ks, 0, sizeof(ks));
@@ -700,6 +773,9 @@ extern "C" int vm_sample(const VmSampleObject* objects, int n_objects, const VmK
   ks.ok = const_cast<uint8_t*>(out->ray_ok);
   ks.points = p.encode ? nullptr : const_cast<float*>(out->points);
   ks.p64 = p.encode ? reinterpret_cast<double*>(ws + pl.off_p64) : nullptr;
+  ks.streams = reinterpret_cast<Stream*>(ws + pl.off_streams);
+  ks.kf = reinterpret_cast<int*>(ws + pl.off_kf);
+  ks.bases = reinterpret_cast<int64_t*>(ws + pl.off_bases);
   ks.nrm = reinterpret_cast<double*>(ws + pl.off_nrm);
   ks.status = reinterpret_cast<int*>(ws + pl.off_status);
   if (aux) {
@@ -709,9 +785,13 @@ extern "C" int vm_sample(const VmSampleObject* objects, int n_objects, const VmK
     ks.aux_t64 = aux->t64;
   }
   cudaStream_t s = cudaStream_t(stream);
-  VM_CUDA(cudaFuncSetAttribute(sample_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pl.smem)));
-  sample_kernel<<<n_objects, kST, pl.smem, s>>>(ks);
+  VM_CUDA(cudaFuncSetAttribute(sample_prep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pl.smem)));
+  sample_prep_kernel<<<n_objects, kST, pl.smem, s>>>(ks);
   VM_CUDA(cudaGetLastError());
+  const int64_t n_rays = int64_t(n_objects) * p.n_rays;
+  sample_rays_kernel<<<unsigned((n_rays + kRT - 1) / kRT), kRT, 0, s>>>(ks, n_objects);
+  VM_CUDA(cudaGetLastError());
+  vm_profile_count_kernels(2);
   if (p.encode) {
     const int D = (p.include_input ? 3 : 0) + 6 * p.n_freq;
     const int64_t spo = int64_t(p.n_rays) * pl.S;
@@ -721,6 +801,7 @@ extern "C" int vm_sample(const VmSampleObject* objects, int n_objects, const VmK
     encode_kernel<<<unsigned((work + 255) / 256), 256, 0, s>>>(n, p.n_freq, p.include_input, D, pl.S, spo, objects,
                                                                ks.p64, const_cast<float*>(out->encoded));
     VM_CUDA(cudaGetLastError());
+    vm_profile_count_kernels(1);
   }
   return VM_OK;
 }

@@ -58,44 +58,84 @@ class KeyframeArena:
         return off
 
 
-def _kf_desc(kf) -> _lib.VmKeyframe:
-    d = _lib.VmKeyframe()
-    d.texel_off = int(kf.texel_off)
-    d.u0, d.v0, d.u1, d.v1 = (int(x) for x in kf.bbox)
-    pose = np.asarray(kf.pose, np.float64)
-    for i in range(3):
-        for j in range(4):
-            d.pose[4 * i + j] = float(pose[i, j])
+KF_DTYPE = np.dtype([("texel_off", "<i8"), ("bbox", "<i4", 4), ("pose", "<f8", 12)])
+OBJ_DTYPE = np.dtype([("object_id", "<i8"), ("kf_begin", "<i4"), ("n_kf", "<i4"), ("active", "<i4"),
+                      ("reserved", "<i4"), ("box_min", "<f8", 3), ("box_max", "<f8", 3), ("center", "<f8", 3),
+                      ("half", "<f8", 3), ("pe_scale", "<f8")])
+assert KF_DTYPE.itemsize == C.sizeof(_lib.VmKeyframe) and OBJ_DTYPE.itemsize == C.sizeof(_lib.VmSampleObject)
+
+
+def _kf_desc(kf) -> bytes:
+    """VmKeyframe bytes of one keyframe (cached: pose/bbox/slot never change)."""
+    d = getattr(kf, "_desc", None)
+    if d is None:
+        rec = np.zeros(1, KF_DTYPE)
+        rec["texel_off"] = int(kf.texel_off)
+        rec["bbox"] = np.asarray(kf.bbox, np.int32)
+        rec["pose"] = np.asarray(kf.pose, np.float64)[:3, :4].reshape(12)
+        d = rec.tobytes()
+        kf._desc = d
     return d
 
 
-def build_tables(arena: KeyframeArena, instances, bound_pad: float, frozen=None, device=DEVICE):
+class DeviceTable:
+    """Persistent device byte buffer refreshed in place (graph-safe: the
+    pointer only changes when the table outgrows it)."""
+
+    def __init__(self, device):
+        self.device = device
+        self.buf = None
+        self.pinned = None
+
+    def upload(self, raw: bytes) -> torch.Tensor:
+        n = len(raw)
+        if self.buf is None or self.buf.numel() < n:
+            cap = max(256, 1 << (n - 1).bit_length())
+            self.buf = torch.zeros(cap, dtype=torch.uint8, device=self.device)
+            self.pinned = torch.zeros(cap, dtype=torch.uint8, pin_memory=True)
+        self.pinned[:n].numpy()[:] = np.frombuffer(raw, dtype=np.uint8)
+        self.buf[:n].copy_(self.pinned[:n], non_blocking=True)
+        return self.buf
+
+
+def build_tables(arena: KeyframeArena, instances, bound_pad: float, frozen=None, device=DEVICE, dest=None):
     """(keyframe table, object table) device byte tensors for instances in
     model-index order.  Each instance's keyframes are laid out contiguously;
     inactive / frozen / keyframe-less instances get a zero batch
-    (trainer.py:272-273, :336-338).  Crops not yet in the arena are uploaded."""
-    kfs = []
-    objs = (_lib.VmSampleObject * max(len(instances), 1))()
+    (trainer.py:272-273, :336-338).  Crops not yet in the arena are uploaded.
+    The padded box follows geometry.py:40-42 (pad = f * half_extent)."""
+    n = len(instances)
+    objs = np.zeros(max(n, 1), OBJ_DTYPE)
+    parts = []
+    begin = 0
+    mins = np.empty((n, 3))
+    maxs = np.empty((n, 3))
     for k, inst in enumerate(instances):
-        o = objs[k]
-        o.object_id = int(inst.object_id)
-        o.kf_begin = len(kfs)
-        for kf in inst.keyframes:
+        kfs = inst.keyframes
+        for kf in kfs:
             if getattr(kf, "texel_off", -1) < 0:
                 arena.add(kf)
-            kfs.append(_kf_desc(kf))
-        o.n_kf = len(inst.keyframes)
-        live = bool(inst.active) and not (frozen is not None and bool(frozen[k]))
-        o.active = 1 if live else 0
-        box = inst.aabb.padded(bound_pad)        # geometry.py:40-42
-        c, h = box.center, box.half_extent
-        for i in range(3):
-            o.box_min[i], o.box_max[i] = float(box.min[i]), float(box.max[i])
-            o.center[i], o.half[i] = float(c[i]), float(h[i])
-        o.pe_scale = float(inst.pe_scale)
-    kf_arr = (_lib.VmKeyframe * max(len(kfs), 1))(*kfs) if kfs else (_lib.VmKeyframe * 1)()
-    to_dev = lambda a: torch.from_numpy(np.frombuffer(bytes(a), dtype=np.uint8).copy()).to(device)
-    return to_dev(kf_arr), to_dev(objs)
+            parts.append(_kf_desc(kf))
+        objs["kf_begin"][k] = begin
+        objs["n_kf"][k] = len(kfs)
+        begin += len(kfs)
+        mins[k] = inst.aabb.min
+        maxs[k] = inst.aabb.max
+        objs["object_id"][k] = inst.object_id
+        objs["active"][k] = 1 if (inst.active and not (frozen is not None and frozen[k])) else 0
+        objs["pe_scale"][k] = inst.pe_scale
+    if n:
+        pad = bound_pad * (0.5 * (maxs - mins))
+        pmin, pmax = mins - pad, maxs + pad
+        objs["box_min"][:n], objs["box_max"][:n] = pmin, pmax
+        objs["center"][:n] = 0.5 * (pmin + pmax)
+        objs["half"][:n] = 0.5 * (pmax - pmin)
+    kf_raw = b"".join(parts) if parts else bytes(KF_DTYPE.itemsize)
+    obj_raw = objs.tobytes()
+    if dest is not None:  # (DeviceTable, DeviceTable): refresh in place
+        return dest[0].upload(kf_raw), dest[1].upload(obj_raw)
+    to_dev = lambda raw: torch.from_numpy(np.frombuffer(raw, dtype=np.uint8).copy()).to(device)
+    return to_dev(kf_raw), to_dev(obj_raw)
 
 
 def sample_params(intr, sampling, seed: int, step: int, n_rays: int, arch, encode: bool) -> _lib.VmSampleParams:

@@ -17,7 +17,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .keyframes import KeyframeArena, SampleBuffers, build_tables, run_sampler, sample_params
+from .keyframes import DeviceTable, KeyframeArena, SampleBuffers, build_tables, run_sampler, sample_params
 from .models import DEVICE, append_model, init_stacked, set_frozen
 from .objects import ObjectMap, add_keyframe
 from .render import CameraIntrinsics
@@ -29,7 +29,8 @@ class Mapper:
     """Owns the object map and both model stacks (trainer.py:203-222)."""
 
     def __init__(self, intrinsics: CameraIntrinsics, cfg: TrainConfig | None = None, device=DEVICE,
-                 object_id_base: int = 0, init_index_base: int = 0, background_init_index: int = 0):
+                 object_id_base: int = 0, init_index_base: int = 0, background_init_index: int = 0,
+                 use_graphs: bool = True):
         self.cfg = cfg if cfg is not None else TrainConfig()
         self.intrinsics = intrinsics
         self.device = torch.device(device)
@@ -55,6 +56,11 @@ class Mapper:
         self._buf_obj = None
         self._buf_bg = None
         self._host_out = None
+        self.use_graphs = use_graphs
+        self._g = None          # graph-replay state (see _graph_step)
+        self._dev_tables = [(DeviceTable(self.device), DeviceTable(self.device)) for _ in range(2)]
+        self._dirty = True
+        self._n_kf = 0
 
     # ------------------------------------------------------------ building
     def add_background(self, aabb, pe_scale: float | None = None):
@@ -79,8 +85,10 @@ class Mapper:
         return kf
 
     def invalidate(self) -> None:
-        """Force the device tables to be rebuilt (after editing boxes/keyframes)."""
-        self._sig = None
+        """Force the device tables to be rebuilt (after editing boxes/keyframes,
+        as process_frame does); the captured step graphs stay valid because the
+        tables are refreshed in place."""
+        self._dirty = True
 
     def freeze_object(self, object_id: int, frozen: bool = True) -> None:
         inst = self.map.instances[object_id]
@@ -93,25 +101,30 @@ class Mapper:
 
     # ------------------------------------------------------------ device sync
     def _signature(self):
-        objs = [self.map.instances[o] for o in self.model_to_object]
+        """Cheap structural signature: model counts, keyframe count, frozen bits."""
+        n_kf = sum(len(self.map.instances[o].keyframes) for o in self.model_to_object) if self._dirty else self._n_kf
         bg = self.map.background
-        return (len(objs), sum(len(i.keyframes) for i in objs), bg is not None,
-                len(bg.keyframes) if bg is not None else 0,
+        return (len(self.model_to_object), n_kf, bg is not None, len(bg.keyframes) if bg is not None else 0,
                 self.obj_params.frozen[:self.obj_params.count].tobytes(),
                 self.bg_params.frozen[:self.bg_params.count].tobytes())
 
     def _sync(self) -> None:
+        if not self._dirty and self._sig is not None:
+            # fast path: only the frozen bits can change behind our back
+            if (self.obj_params.frozen[:self.obj_params.count].tobytes() == self._sig[4]
+                    and self.bg_params.frozen[:self.bg_params.count].tobytes() == self._sig[5]):
+                return
         sig = self._signature()
-        if sig == self._sig:
-            return
         c = self.cfg
         S = c.points_per_ray
         objs = [self.map.instances[o] for o in self.model_to_object]
+        self._n_kf = sum(len(i.keyframes) for i in objs)
         pad = c.association.bound_pad
-        t_obj = build_tables(self.arena, objs, pad, self.obj_params.frozen, self.device) if objs else None
+        t_obj = build_tables(self.arena, objs, pad, self.obj_params.frozen, self.device,
+                             dest=self._dev_tables[0]) if objs else None
         bg = self.map.background
         t_bg = build_tables(self.arena, [bg], pad, self.bg_params.frozen[bg.model_index:bg.model_index + 1],
-                            self.device) if bg is not None else None
+                            self.device, dest=self._dev_tables[1]) if bg is not None else None
         K = len(objs)
         if K and (self._buf_obj is None or self._buf_obj.K != K):
             self._buf_obj = SampleBuffers(K, c.rays_per_object, S, c.arch_object.input_dim, False, self.device)
@@ -121,8 +134,14 @@ class Mapper:
             self._buf_obj.pe_scale[:K] = torch.tensor([float(i.pe_scale) for i in objs], device=self.device)
         if bg is not None:
             self._buf_bg.pe_scale[:1] = float(bg.pe_scale)
+        if self._g is not None:  # keep the graphs' second batch buffers' PE scales in step
+            for a, b in zip(self._g["bufs"], (self._buf_obj, self._buf_bg)):
+                if a is not None and b is not None:
+                    a.pe_scale.copy_(b.pe_scale)
+            self._g["next_ready"] = None  # tables changed: drop the prefetched batch
         self._tables = (t_obj, t_bg)
         self._sig = sig
+        self._dirty = False
         up = sum(t.numel() for tab in self._tables if tab is not None for t in tab) + 4 * (K + (bg is not None))
         self._io = (up, self._io[1])
 
@@ -170,6 +189,139 @@ class Mapper:
         losses, status = launch_train(stacks, c.loss_weights, self._ws)
         return losses, status, stacks
 
+    # ------------------------------------------------------------ graph replay
+    def _graph_key(self):
+        tabs = tuple(t.data_ptr() for tab in self._tables if tab is not None for t in tab)
+        bufs = tuple(b.t.data_ptr() for b in (self._buf_obj, self._buf_bg) if b is not None)
+        return (self._sig, tabs, bufs, self.obj_params.arena.data_ptr(), self.bg_params.arena.data_ptr(),
+                self.obj_params.count, self.bg_params.count, self.cfg.train_background)
+
+    def _build_graphs(self):
+        """Capture two CUDA graphs (step parity p = 0, 1).  Graph p trains
+        step t from batch buffer p while a forked stream samples step t+1 into
+        buffer 1-p (the sampler only reads keyframes, never parameters, so it
+        overlaps training); then it copies losses/status to pinned host memory
+        and bumps the device step counter."""
+        c = self.cfg
+        dev = self.device
+        objs_n = self.obj_params.count
+        bg = self.map.background
+        has_bg = c.train_background and bg is not None
+        S = c.points_per_ray
+        bufs_o = [self._buf_obj, SampleBuffers(objs_n, c.rays_per_object, S, c.arch_object.input_dim, False, dev)
+                  ] if objs_n else [None, None]
+        bufs_b = [self._buf_bg, SampleBuffers(1, c.rays_background, S, c.arch_background.input_dim, False, dev)
+                  ] if has_bg else [None, None]
+        if objs_n:
+            bufs_o[1].pe_scale.copy_(bufs_o[0].pe_scale)
+        if has_bg:
+            bufs_b[1].pe_scale.copy_(bufs_b[0].pe_scale)
+        step_dev = torch.zeros(1, dtype=torch.int64, device=dev)
+        t_obj, t_bg = self._tables
+
+        def sample(p, offset):
+            if objs_n:
+                sp = sample_params(self.intrinsics, c.sampling, c.seed, 0, c.rays_per_object, c.arch_object, False)
+                sp.step_dev, sp.step_offset = step_dev.data_ptr(), offset
+                run_sampler(self.arena, t_obj[0], t_obj[1], objs_n, sp, bufs_o[p])
+            if has_bg:
+                sp = sample_params(self.intrinsics, c.sampling, c.seed, 0, c.rays_background, c.arch_background,
+                                   False)
+                sp.step_dev, sp.step_offset = step_dev.data_ptr(), offset
+                run_sampler(self.arena, t_bg[0], t_bg[1], 1, sp, bufs_b[p])
+
+        def stacks(p):
+            out = []
+            if objs_n:
+                out.append((self.obj_params, self.obj_state, bufs_o[p]))
+            if has_bg:
+                out.append((self.bg_params, self.bg_state, bufs_b[p]))
+            return out
+
+        # eager warm-up of both buffers/workspaces (allocations must precede capture)
+        for p in (0, 1):
+            sample(p, 0)
+        launch_train(stacks(0), c.loss_weights, self._ws, bump_version=False)  # state restored by caller
+        torch.cuda.synchronize(dev)
+        n = sum(p.count for p, _, _ in stacks(0))
+        host_l = torch.empty((n, 3), dtype=torch.float32, pin_memory=True)
+        host_s = torch.empty(4 * len(stacks(0)), dtype=torch.int32, pin_memory=True)
+        side = torch.cuda.Stream(dev)
+        graphs = []
+        for p in (0, 1):
+            g = torch.cuda.CUDAGraph()
+            main = torch.cuda.Stream(dev)
+            with torch.cuda.stream(main):
+                with torch.cuda.graph(g, stream=main):
+                    cur = torch.cuda.current_stream()
+                    side.wait_stream(cur)
+                    with torch.cuda.stream(side):
+                        sample(1 - p, 1)
+                    losses, status = launch_train(stacks(p), c.loss_weights, self._ws, bump_version=False)
+                    host_l.copy_(losses, non_blocking=True)
+                    host_s.copy_(status, non_blocking=True)
+                    cur.wait_stream(side)
+                    _lib.check(_lib.load().vm_step_advance(step_dev.data_ptr(), 1, _lib.stream_ptr()),
+                               "vm_step_advance")
+            graphs.append(g)
+        self._g = dict(key=self._graph_key(), graphs=graphs, step_dev=step_dev, host_l=host_l, host_s=host_s,
+                       stacks=[stacks(0), stacks(1)], sample=sample, next_ready=None,
+                       bufs=(bufs_o[1], bufs_b[1]))
+
+    def enqueue_graph_step(self, step: int):
+        """Replay the captured step graph for `step` on the current stream
+        (no host sync).  Results land in pinned host memory when the stream
+        reaches them."""
+        self._sync()
+        if self._g is None or self._g["key"] != self._graph_key():
+            self._snapshot_for_graph_build()
+            self._build_graphs()
+            self._restore_after_graph_build()
+        g = self._g
+        p = step & 1
+        g["step_dev"].fill_(step)
+        if g["next_ready"] != step:  # no prefetched batch for this step: sample it now
+            g["sample"](p, 0)
+        g["graphs"][p].replay()
+        g["next_ready"] = step + 1
+        for params, _, _ in g["stacks"][p]:
+            params.version += 1
+        return g["stacks"][p]
+
+    def _graph_step(self, step: int):
+        stacks = self.enqueue_graph_step(step)
+        torch.cuda.current_stream().synchronize()
+        g = self._g
+        return g["host_l"].numpy(), g["host_s"].numpy().reshape(-1, 4), stacks
+
+    def _snapshot_for_graph_build(self):
+        """Graph capture needs one eager warm-up launch; keep the model state
+        untouched by saving/restoring params, Adam moments and step counters."""
+        self._sync()
+        snap = []
+        for p, s in ((self.obj_params, self.obj_state), (self.bg_params, self.bg_state)):
+            snap.append((p.arena.clone(), s.m_arena.clone(), s.v_arena.clone(), s.step.clone(), p.version))
+        self._snap = snap
+
+    def _restore_after_graph_build(self):
+        for (a, m, v, st, ver), (p, s) in zip(self._snap, ((self.obj_params, self.obj_state),
+                                                        (self.bg_params, self.bg_state))):
+            p.arena.copy_(a)
+            s.m_arena.copy_(m)
+            s.v_arena.copy_(v)
+            s.step.copy_(st)
+            p.version = ver
+        self._snap = None
+        torch.cuda.synchronize(self.device)
+
+    def kernels_per_step(self) -> int:
+        """Kernels of ours one graph-replayed step launches: per stack a sampler
+        prep + ray kernel, plus the fused MLP, Adam, the partial reduce when a
+        model is split over CTAs, and the step-counter bump."""
+        n_st = (self.obj_params.count > 0) + (self.cfg.train_background and self.map.background is not None)
+        split = 1 if (self.cfg.train_background and self.map.background is not None) else 0
+        return 2 * n_st + 2 + split + 1
+
     def last_io_bytes(self) -> tuple[int, int]:
         """(host->device bytes of the last table upload, device->host bytes per step)."""
         return self._io
@@ -180,10 +332,15 @@ class Mapper:
             raise ValueError(f"unknown training mode {mode!r}")
         step = self.global_step
         t0 = time.perf_counter()
-        losses, status, stacks = self.enqueue_step(step)
         report_losses: dict[int, tuple[float, float, float]] = {}
         k_models = 0
-        if stacks:
+        self._sync()
+        has_work = self.obj_params.count > 0 or (self.cfg.train_background and self.map.background is not None)
+        if has_work and self.use_graphs and mode == "vectorised":
+            l, st, stacks = self._graph_step(step)
+            self._io = (self._io[0], l.nbytes + st.nbytes)
+        elif has_work:
+            losses, status, stacks = self.enqueue_step(step)
             n = losses.shape[0]
             packed = torch.cat([losses.reshape(-1).view(torch.int32), status])
             if self._host_out is None or self._host_out.numel() != packed.numel():
@@ -193,20 +350,22 @@ class Mapper:
             host = self._host_out.numpy()
             l = host[:3 * n].view(np.float32).reshape(n, 3)
             st = host[3 * n:].reshape(-1, 4)
-            row = 0
-            for si, (params, _, _) in enumerate(stacks):
-                is_bg = params is self.bg_params
-                kk = params.count
-                if st[si, 0] < kk:
-                    raise FloatingPointError(f"non-finite gradient for model index {int(st[si, 0])}")
-                for j in range(kk):
-                    oid = 0 if is_bg else self.model_to_object[j]
-                    vals = l[row + j]
-                    if not np.all(np.isfinite(vals)):
-                        raise FloatingPointError(f"non-finite loss for object {oid}")
-                    report_losses[oid] = (float(vals[0]), float(vals[1]), float(vals[2]))
-                row += kk
-                k_models += kk
+        else:
+            stacks = []
+        row = 0
+        for si, (params, _, _) in enumerate(stacks):
+            is_bg = params is self.bg_params
+            kk = params.count
+            if st[si, 0] < kk:
+                raise FloatingPointError(f"non-finite gradient for model index {int(st[si, 0])}")
+            vals = l[row:row + kk]
+            ids = [0] if is_bg else self.model_to_object
+            if st[si, 1] < kk or not np.isfinite(vals).all():
+                bad = int(np.flatnonzero(~np.isfinite(vals).all(axis=1))[0])
+                raise FloatingPointError(f"non-finite loss for object {ids[bad]}")
+            report_losses.update(zip(ids, map(tuple, vals.astype(np.float64).tolist())))
+            row += kk
+            k_models += kk
         w = self.cfg.loss_weights
         total = sum(d + w.colour * c + w.occupancy * o for d, c, o in report_losses.values())
         self.global_step += 1

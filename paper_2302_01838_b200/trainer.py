@@ -130,7 +130,7 @@ class TrainWorkspace:
 _default_ws = TrainWorkspace()
 
 
-def launch_train(stacks, weights: LossWeights, ws: TrainWorkspace | None = None):
+def launch_train(stacks, weights: LossWeights, ws: TrainWorkspace | None = None, bump_version: bool = True):
     """Enqueue one fused step for [(params, state, batch), ...] (no host sync).
 
     Returns (losses [sum K, 3] device tensor, status device tensor).
@@ -153,8 +153,9 @@ def launch_train(stacks, weights: LossWeights, ws: TrainWorkspace | None = None)
     ws.ensure(nbytes, kt, n, dev)
     _lib.check(lib.vm_train_step(vs, vb, n, weights.vm(), ws.losses.data_ptr(), ws.status.data_ptr(),
                                  ws.ws.data_ptr(), ws.ws.numel(), _lib.stream_ptr()), "train_on_batch")
-    for p, _, _ in stacks:
-        p.version += 1
+    if bump_version:
+        for p, _, _ in stacks:
+            p.version += 1
     return ws.losses[:kt], ws.status[:4 * n]
 
 

@@ -1,0 +1,65 @@
+"""Write profiles/<tag>_summary.md (+ traffic.json) from ncu reports in gpurun_out/."""
+import csv
+import json
+import subprocess
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parents[1]
+tag = sys.argv[1] if len(sys.argv) > 1 else "r01"
+out = ROOT / "profiles"
+out.mkdir(exist_ok=True)
+KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+        "sm__throughput.avg.pct_of_peak_sustained_elapsed", "gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed",
+        "sm__warps_active.avg.pct_of_peak_sustained_active", "smsp__issue_active.avg.pct_of_peak_sustained_active",
+        "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active",
+        "smsp__sass_thread_inst_executed_op_ffma_pred_on.sum.per_cycle_elapsed",
+        "sm__sass_thread_inst_executed_op_ffma_pred_on.sum.peak_sustained",
+        "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "smsp__sass_inst_executed_op_shared_ld.sum",
+        "smsp__inst_executed.sum", "launch__registers_per_thread", "launch__shared_mem_per_block_dynamic",
+        "launch__grid_size", "launch__block_size", "lts__t_sector_hit_rate.pct"]
+
+
+def raw(rep):
+    txt = subprocess.run(["ncu", "-i", str(rep), "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(txt.splitlines()))
+    hdr, units, vals = rows[0], rows[1], rows[2]
+    return {k: (v, u) for k, u, v in zip(hdr, units, vals)}
+
+
+def stalls(d):
+    st = [(float(v.replace(",", "")), k) for k, (v, u) in d.items()
+          if k.startswith("smsp__pcsamp_warps_issue_stalled_") and not k.endswith("not_issued")]
+    tot = sum(v for v, _ in st) or 1
+    return [(k[33:], 100 * v / tot) for v, k in sorted(st, reverse=True)[:8]]
+
+
+lines = [f"# ncu summary ({tag})", "",
+         "Captured with `ncu --set full --clock-control none --import-source on` on one B200 under gpurun,",
+         "command `python bench.py --steps 2 --warmup 3 --no-cpu-baseline` (config 2), one launch per kernel.",
+         "ncu flushes caches before each replay: durations are cold-cache and serialised.", ""]
+traffic = {}
+for name, rep in (("fused MLP train (KF, mlp_kernel)", "prof_mlp"), ("sampler rays (KS)", "prof_rays"),
+                  ("Adam (KA)", "prof_adam")):
+    p = ROOT / "gpurun_out" / f"{rep}.ncu-rep"
+    if not p.exists():
+        continue
+    d = raw(p)
+    lines += [f"## {name}", "", "| metric | value | unit |", "|---|---|---|"]
+    for k in KEYS:
+        if k in d:
+            lines.append(f"| {k} | {d[k][0]} | {d[k][1]} |")
+    lines += ["", "Top warp stall reasons (share of samples): " +
+              ", ".join(f"{k} {v:.1f}%" for k, v in stalls(d)), ""]
+    if rep == "prof_mlp":
+        mb = lambda k: float(d[k][0].replace(",", "")) * (1e6 if d[k][1] == "Mbyte" else 1e3 if d[k][1] == "Kbyte" else 1)
+        traffic["mlp_kernel_dram_bytes_per_launch"] = mb("dram__bytes_read.sum") + mb("dram__bytes_write.sum")
+        traffic["source"] = f"profiles/{tag}_summary.md (ncu --set full, cold cache)"
+summ = ROOT / "gpurun_out" / "launches_summary.txt"
+if summ.exists():
+    lines += ["## Launch list (ncu --metrics gpu__time_duration.sum, per-step kernels)", "", "```",
+              summ.read_text().rstrip(), "```", ""]
+(out / f"{tag}_summary.md").write_text("\n".join(lines) + "\n")
+if traffic:
+    (out / "traffic.json").write_text(json.dumps(traffic, indent=1) + "\n")
+print("\n".join(lines))

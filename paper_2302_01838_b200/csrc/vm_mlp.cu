@@ -3,6 +3,7 @@
 #include "vm_mlp.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -121,6 +122,12 @@ __device__ void finalize_model(const KStack& st, int k, bool all_finite, bool me
   }
 }
 
+}  // namespace vm
+
+#include "vm_tc_mlp.cuh"
+
+namespace vm {
+
 constexpr int kRedThreads = 128;
 constexpr int kRedLanes = 4;                                  // lanes per float4 of output
 constexpr int kRedChunk = kRedThreads / kRedLanes * 4;        // floats per reduce CTA
@@ -184,6 +191,9 @@ __global__ void __launch_bounds__(kRedThreads) reduce_partials_kernel(const __gr
   }
   const bool all_finite = __syncthreads_and(finite);
   finalize_model(st, k, all_finite, ch == 0, red_smem, st.R * 3);
+#ifdef VM_TC_DEBUG
+  if (threadIdx.x == 0) atomicAdd(&vm_tc_dbg[65], 1);
+#endif
 }
 
 template <int H, int L, int MODE>
@@ -471,6 +481,9 @@ __global__ void __launch_bounds__(256) adam_train_kernel(const __grid_constant__
   const int i = (ch * 256 + threadIdx.x) * 4;
   if (i < s.block) adam_vec4(s.P + base, s.M + base, s.V + base, s.G + base, i, c.x, c.y, s.a);
   if (ch == 0 && threadIdx.x == 0) s.step[k] += 1;
+#ifdef VM_TC_DEBUG
+  if (threadIdx.x == 0) atomicAdd(&vm_tc_dbg[66], 1);
+#endif
 }
 
 // ------------------------------------------------------------------ host side
@@ -559,6 +572,12 @@ static int blocks_per_split(int nblk, int p) {
 static int choose_splits(const KStack* ks, int n, int* P) {
   int nblk[2], total = 0;
   for (int i = 0; i < n; ++i) {
+    if (ks[i].tc) {
+      const int g = tck::kTM / ks[i].S;
+      P[i] = std::max(1, (ks[i].R + g - 1) / g);
+      nblk[i] = 0;
+      continue;
+    }
     const double flop_per_sample = double(ks[i].H) * (ks[i].Dp + 2 * (ks[i].L - 2) * ks[i].H + 8) * 3.0;
     const double cost = flop_per_sample * ks[i].R * ks[i].S;
     nblk[i] = (ks[i].R + ks[i].G - 1) / ks[i].G;
@@ -568,7 +587,7 @@ static int choose_splits(const KStack* ks, int n, int* P) {
   }
   // Keep a multi-stack launch within one wave of 148 SMs: a second wave of a
   // few CTAs doubles the kernel time.  Shrink the most-split stack to fit.
-  if (n > 1 && total > kSMs) {
+  if (n > 1 && total > kSMs && !ks[0].tc && !ks[1].tc) {
     int big = ks[0].K * P[0] >= ks[1].K * P[1] ? 0 : 1;
     const int others = total - ks[big].K * P[big];
     const int budget = (kSMs - others) / std::max(1, ks[big].K);
@@ -609,10 +628,20 @@ struct TrainPlan {
   size_t smem;
   size_t ws_bytes;
   // workspace offsets
-  size_t off_grads[2], off_part[2], off_terms[2], off_cnt[2], off_upd[2], off_corr[2];
+  size_t off_grads[2], off_part[2], off_terms[2], off_cnt[2], off_upd[2], off_corr[2], off_img[2];
 };
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// The tensor-core path is the default for hidden-128 stacks; VM_TC=0 selects
+// the FFMA kernel for them (A/B measurements and the parity cross-check).
+bool tc_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("VM_TC");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
 
 int plan_train(const VmStack* stacks, const VmBatch* batches, int n, TrainPlan& pl) {
   VM_REQUIRE(n >= 1 && n <= 2, "vm_train_step: 1 or 2 stacks supported");
@@ -650,6 +679,7 @@ int plan_train(const VmStack* stacks, const VmBatch* batches, int n, TrainPlan& 
     ks.tmask = b.target_mask;
     ks.valid = b.valid_depth;
     ks.ok = b.ray_ok;
+    ks.tc = tc_enabled() && ks.H == 128 && ks.L == 4 && ks.D <= tck::kK0 && ks.S <= 32 ? 1 : 0;
   }
   choose_splits(pl.kp.s, n, P);
   for (int i = 0; i < n; ++i) {
@@ -666,7 +696,8 @@ int plan_train(const VmStack* stacks, const VmBatch* batches, int n, TrainPlan& 
     pl.off_cnt[i] = off;   off = align_up(off + K * 4, 256);
     pl.off_upd[i] = off;   off = align_up(off + K, 256);
     pl.off_corr[i] = off;  off = align_up(off + K * 8, 256);
-    pl.smem = std::max(pl.smem, smem_bytes(ks));
+    pl.off_img[i] = off;   off = align_up(off + (ks.tc ? K * tck::Img<128, 4>::total * 4 : 0), 256);
+    if (!ks.tc) pl.smem = std::max(pl.smem, smem_bytes(ks));
     AdamStack& as = pl.ap.s[i];
     as.P = stacks[i].params;
     as.M = stacks[i].m;
@@ -723,9 +754,22 @@ extern "C" int vm_train_step(const VmStack* stacks, const VmBatch* batches, int 
     as.status = ks.status;
   }
   if (pl.grid == 0) return VM_OK;
-  KernelFn fn = pick_kernel<kTrain>(pl.kp.s[0].H, pl.kp.s[0].L, n_stacks > 1 ? pl.kp.s[1].H : 0,
-                                    n_stacks > 1 ? pl.kp.s[1].L : 0);
-  if (!fn) {
+  // FFMA kernel over the stacks KT does not take
+  KParams kf;
+  std::memset(&kf, 0, sizeof(kf));
+  int ff_grid = 0;
+  for (int i = 0; i < n_stacks; ++i) {
+    if (pl.kp.s[i].tc) continue;
+    kf.s[kf.n_stacks] = pl.kp.s[i];
+    kf.s[kf.n_stacks].item_base = ff_grid;
+    ff_grid += pl.kp.s[i].K * pl.kp.s[i].P;
+    kf.n_stacks++;
+  }
+  KernelFn fn = nullptr;
+  if (kf.n_stacks > 0) {
+    fn = pick_kernel<kTrain>(kf.s[0].H, kf.s[0].L, kf.n_stacks > 1 ? kf.s[1].H : 0, kf.n_stacks > 1 ? kf.s[1].L : 0);
+  }
+  if (kf.n_stacks > 0 && !fn) {
     if (n_stacks == 2) {  // no fused instantiation for this pair: run stacks back to back
       // (Adam of stack 1 still honours stack 0's status because both read it)
       set_error("vm_train_step: unsupported stack pair");
@@ -740,9 +784,24 @@ extern "C" int vm_train_step(const VmStack* stacks, const VmBatch* batches, int 
     e1 = g_prof.get();
     VM_CUDA(cudaEventRecord(e0, s));
   }
-  rc = launch_mlp(fn, pl.kp, pl.grid, pl.smem, s);
-  if (rc) return rc;
-  if (g_prof.on) g_prof.kernels += 1;
+  for (int i = 0; i < n_stacks; ++i) {
+    const KStack& ks = pl.kp.s[i];
+    if (!ks.tc || ks.K == 0) continue;
+    using I = tck::Img<128, 4>;
+    float* img = reinterpret_cast<float*>(ws + pl.off_img[i]);
+    tck::tc_prep_kernel<128, 4><<<dim3(I::n_chunks, ks.K), 256, 0, s>>>(ks, img);
+    VM_CUDA(cudaGetLastError());
+    const int smem_tc = tck::Smem<128, 4>::total;
+    VM_CUDA(cudaFuncSetAttribute(tck::tc_train_kernel<128, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_tc));
+    tck::tc_train_kernel<128, 4><<<ks.K * ks.P, tck::kTCThreads, smem_tc, s>>>(pl.kp, i, img);
+    VM_CUDA(cudaGetLastError());
+    if (g_prof.on) g_prof.kernels += 2;
+  }
+  if (fn) {
+    rc = launch_mlp(fn, kf, ff_grid, pl.smem, s);
+    if (rc) return rc;
+    if (g_prof.on) g_prof.kernels += 1;
+  }
   if (g_prof.on) VM_CUDA(cudaEventRecord(e1, s));
   int red_grid = 0;
   for (int i = 0; i < n_stacks; ++i)
@@ -817,6 +876,19 @@ extern "C" int vm_backward(const VmStack* st, const float* encoded, int64_t n_sa
                            const float* grad_col, float* grads, void* stream) {
   return run_fwd_bwd(st, encoded, n_samples, grad_occ, grad_col, nullptr, nullptr, grads, true,
                      cudaStream_t(stream));
+}
+
+extern "C" int vm_tc_debug_read(int* out) {
+#ifdef VM_TC_DEBUG
+  static cudaStream_t ds = nullptr;
+  if (!ds) cudaStreamCreateWithFlags(&ds, cudaStreamNonBlocking);
+  VM_CUDA(cudaMemcpyFromSymbolAsync(out, vm_tc_dbg, sizeof(int) * 256, 0, cudaMemcpyDeviceToHost, ds));
+  VM_CUDA(cudaStreamSynchronize(ds));
+  return VM_OK;
+#else
+  (void)out;
+  return VM_ERR_UNSUPPORTED;
+#endif
 }
 
 extern "C" int vm_profile_enable(int on) {

@@ -52,6 +52,7 @@ struct KStack {
   int block, w_floats, team_floats;
   int w_off[VM_MAX_LAYERS], b_off[VM_MAX_LAYERS];
   int K, R, S, G, P;          // models, rays, points/ray, rays/block, CTAs per model
+  int tc;                     // 1: trained by the tensor-core kernel KT (vm_tc_mlp.cuh)
   int64_t N;                  // samples per model (forward/backward modes)
   int model_base;             // global model index of model 0 (losses/status)
   int item_base;              // first CTA index of this stack

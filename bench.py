@@ -253,6 +253,11 @@ def main():
     n_launch = C.c_int()
     mlp_ms = C.c_double()
     lib.vm_profile_read(C.byref(n_launch), C.byref(mlp_ms))
+    per_tag = {}
+    for tag in (1, 2):  # 1: FFMA kernel KF (objects), 2: tensor-core branch KT (background)
+        n_t, ms_t = C.c_int(), C.c_double()
+        lib.vm_profile_read_tag(tag, C.byref(n_t), C.byref(ms_t))
+        per_tag[tag] = ms_t.value / n_t.value if n_t.value else None
     lib.vm_profile_enable(0)
     step_ms = sum(a.elapsed_time(b) for a, b in ev)
     t_local = torch.tensor([step_ms], dtype=torch.float64, device=dev)
@@ -286,17 +291,44 @@ def main():
     h2d, d2h = mapper.last_io_bytes()
     h2d = -(-h2d // cfg.steps_per_frame)  # table upload amortised over the frame's steps
 
-    # roofline of the dominant kernel (fused MLP fwd/bwd): algorithmic FLOPs
-    # per launch / CUDA-event duration of that launch inside the timed region.
-    flop_launch = (k_local * cfg.rays_per_object * cfg.points_per_ray * flop_per_sample(32)
-                   + (cfg.rays_background * cfg.points_per_ray * flop_per_sample(128)
-                      if cfg.train_background else 0))
+    # rooflines: algorithmic FLOPs per launch / CUDA-event duration of that
+    # launch (same step, eager replay with L2 flushed).  KF (objects, FP32
+    # FFMA) and KT (background, tcgen05 3xTF32 + its weight-image prep) run
+    # concurrently on two streams; the MLP phase is fork .. join.
+    flop_obj = k_local * cfg.rays_per_object * cfg.points_per_ray * flop_per_sample(32)
+    flop_bg = (cfg.rays_background * cfg.points_per_ray * flop_per_sample(128)) if cfg.train_background else 0
+    flop_launch = flop_obj + flop_bg
     kernel_ms = mlp_ms.value / max(n_launch.value, 1)
-    achieved = flop_launch / (kernel_ms * 1e-3) / 1e12
     traffic = None
     tf_path = ROOT / "profiles" / "traffic.json"
     if tf_path.exists():
         traffic = json.loads(tf_path.read_text()).get("mlp_kernel_dram_bytes_per_launch")
+    peaks_path = ROOT / "MEASURED_PEAKS.json"
+    bf16 = json.loads(peaks_path.read_text()).get("bf16_tflops") if peaks_path.exists() else None
+    tf32_peak = (bf16 if bf16 else 1590.0) / 2.0
+    tf32_src = ("dense TF32 = 1/2 of the measured bf16 cuBLAS burst peak in MEASURED_PEAKS.json" if bf16 else
+                "dense TF32 = 1/2 of the profiling guide's fallback bf16 peak")
+    kernels = []
+    if per_tag.get(1):
+        a = flop_obj / (per_tag[1] * 1e-3) / 1e12
+        kernels.append({"bound": "fp32", "achieved": a, "peak": ffma_peak, "unit": "TFLOP/s", "frac": a / ffma_peak,
+                        "traffic": traffic, "kernel": "mlp_kernel (KF, FFMA, hidden-32 objects)",
+                        "kernel_ms": per_tag[1], "flop_per_launch": flop_obj,
+                        "peak_source": "FP32 FFMA throughput measured in this run by vm_ffma_peak "
+                                       "(MEASURED_PEAKS.json has no FP32 entry)"})
+    if per_tag.get(2) and flop_bg:
+        a = flop_bg / (per_tag[2] * 1e-3) / 1e12
+        kernels.append({"bound": "tensor", "achieved": a, "peak": tf32_peak, "unit": "TFLOP/s", "frac": a / tf32_peak,
+                        "traffic": None, "kernel": "tc_train_kernel (KT, tcgen05 3xTF32, hidden-128 background)",
+                        "kernel_ms": per_tag[2], "flop_per_launch": flop_bg,
+                        "note": "3xTF32 issues 3 MMAs per algorithmic product; tensor-pipe FLOPs = 3x achieved",
+                        "peak_source": tf32_src})
+    if not kernels:  # single FFMA launch (e.g. VM_TC=0): the phase is the kernel
+        a = flop_launch / (kernel_ms * 1e-3) / 1e12
+        kernels.append({"bound": "fp32", "achieved": a, "peak": ffma_peak, "unit": "TFLOP/s", "frac": a / ffma_peak,
+                        "traffic": traffic, "kernel": "mlp_kernel (fused KF)", "kernel_ms": kernel_ms,
+                        "flop_per_launch": flop_launch, "peak_source": "FP32 FFMA throughput measured in this run"})
+    dominant = max(kernels, key=lambda r: r["kernel_ms"])
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -314,11 +346,10 @@ def main():
             "samples_per_s": value * cfg.rays_per_object * cfg.points_per_ray,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "gpu_launches": kernels_per_step * args.steps,
-            "roofline": {"bound": "fp32", "achieved": achieved, "peak": ffma_peak, "unit": "TFLOP/s",
-                         "frac": achieved / ffma_peak, "traffic": traffic, "kernel": "mlp_kernel (fused KF)",
-                         "kernel_ms": kernel_ms, "flop_per_launch": flop_launch,
-                         "peak_source": "FP32 FFMA throughput measured in this run by vm_ffma_peak "
-                                        "(MEASURED_PEAKS.json has no FP32 entry)"},
+            "roofline": dominant,
+            "roofline_kernels": kernels,
+            "mlp_phase": {"ms": kernel_ms, "flop": flop_launch,
+                          "achieved_tflops": flop_launch / (kernel_ms * 1e-3) / 1e12},
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
         }

@@ -101,6 +101,7 @@ _SIGNATURES = {
                             C.c_void_p, C.c_size_t, C.c_void_p]),
     "vm_profile_enable": (C.c_int, [C.c_int]),
     "vm_profile_read": (C.c_int, [C.POINTER(C.c_int), C.POINTER(C.c_double)]),
+    "vm_profile_read_tag": (C.c_int, [C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_double)]),
     "vm_profile_kernels": (C.c_int, [C.POINTER(C.c_long)]),
     "vm_profile_count_kernels": (None, [C.c_int]),
     "vm_train_grid": (C.c_int, [C.POINTER(VmStack), C.POINTER(VmBatch), C.c_int, C.POINTER(C.c_int),

@@ -108,4 +108,82 @@ __device__ __forceinline__ void render_ray_backward(int S, const Occ& occ, const
   }
 }
 
+// Register-resident variant of the whole per-ray chain for a compile-time
+// sample count NS (render_ray_forward + render_ray_sums + ray_loss_grad +
+// render_ray_backward with identical operation order).  With NS known every
+// loop is straight-line code, so the independent per-sample work of the sums
+// and of the backward pass overlaps instead of running as one predicated
+// chain.  On return o[] / c[][] hold the sigmoid-input gradients dz.
+template <int NS>
+__device__ __forceinline__ RayLossGrad render_ray_fixed(float (&o)[NS], float (&c)[3][NS], const float (&t)[NS],
+                                                        const RayTargets& tg, float w_colour, float w_occ) {
+  float T[NS], w[NS];
+  float Tc = 1.0f;
+#pragma unroll
+  for (int i = 0; i < NS; ++i) {
+    T[i] = Tc;
+    Tc = (i == 0) ? __fsub_rn(1.0f, o[0]) : __fmul_rn(Tc, __fsub_rn(1.0f, o[i]));
+    w[i] = __fmul_rn(o[i], T[i]);
+  }
+  // pairwise_sum_leaf (loops_utils.h.src order) for n = NS <= 128
+  auto psum = [&](auto&& get) -> float {
+    if constexpr (NS < 8) {
+      float res = -0.0f;
+#pragma unroll
+      for (int i = 0; i < NS; ++i) res = __fadd_rn(res, get(i));
+      return res;
+    } else {
+      float r[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) r[j] = get(j);
+      constexpr int full = NS - (NS % 8);
+#pragma unroll
+      for (int i = 8; i < full; i += 8)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) r[j] = __fadd_rn(r[j], get(i + j));
+      float res = __fadd_rn(__fadd_rn(__fadd_rn(r[0], r[1]), __fadd_rn(r[2], r[3])),
+                            __fadd_rn(__fadd_rn(r[4], r[5]), __fadd_rn(r[6], r[7])));
+#pragma unroll
+      for (int i = full; i < NS; ++i) res = __fadd_rn(res, get(i));
+      return res;
+    }
+  };
+  RayFwd f;
+  f.opacity = psum([&](int i) { return w[i]; });
+  f.depth = psum([&](int i) { return __fmul_rn(w[i], t[i]); });
+#pragma unroll
+  for (int ch = 0; ch < 3; ++ch) {
+    float acc = __fmul_rn(w[0], c[ch][0]);
+#pragma unroll
+    for (int i = 1; i < NS; ++i) acc = __fadd_rn(acc, __fmul_rn(w[i], c[ch][i]));
+    f.colour[ch] = acc;
+  }
+  const RayLossGrad lg = ray_loss_grad(f, tg, w_colour, w_occ);
+  float g[NS], gw[NS];
+#pragma unroll
+  for (int i = 0; i < NS; ++i) {
+    float cs = __fmul_rn(lg.dC[0], c[0][i]);
+    cs = __fadd_rn(cs, __fmul_rn(lg.dC[1], c[1][i]));
+    cs = __fadd_rn(cs, __fmul_rn(lg.dC[2], c[2][i]));
+    g[i] = __fadd_rn(__fadd_rn(lg.dO, __fmul_rn(lg.dD, t[i])), cs);
+    gw[i] = __fmul_rn(g[i], w[i]);
+  }
+  float rev = 0.0f;
+#pragma unroll
+  for (int i = NS - 1; i >= 0; --i) {
+    rev = (i == NS - 1) ? gw[i] : __fadd_rn(rev, gw[i]);
+    const float suffix = __fsub_rn(rev, gw[i]);
+    const float denom = np_maximum(__fsub_rn(1.0f, o[i]), 1e-7f);
+    const float d_occ = __fsub_rn(__fmul_rn(g[i], T[i]), __fdiv_rn(suffix, denom));
+    const float oi = o[i];
+    o[i] = __fmul_rn(__fmul_rn(d_occ, oi), __fsub_rn(1.0f, oi));
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) {
+      const float cv = c[ch][i];
+      c[ch][i] = __fmul_rn(__fmul_rn(__fmul_rn(w[i], lg.dC[ch]), cv), __fsub_rn(1.0f, cv));
+    }
+  }
+  return lg;
+}
+
 }  // namespace vm

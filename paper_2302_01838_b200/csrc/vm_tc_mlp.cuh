@@ -36,18 +36,23 @@
 #include "vm_tc.cuh"
 
 #ifdef VM_TC_DEBUG
-__device__ int vm_tc_dbg[256];
+__device__ int vm_tc_dbg[512];
 #define VM_TC_DBG(i, v) \
   do { if (blockIdx.x == 0 && (threadIdx.x & 31) == 0) reinterpret_cast<volatile int*>(vm_tc_dbg)[i] = (v); } while (0)
 #else
 #define VM_TC_DBG(i, v) do { } while (0)
+#endif
+#ifdef VM_TC_DEBUG
+#define VM_TC_T(ev) \
+  do { if (blockIdx.x == 0 && threadIdx.x == 0) { reinterpret_cast<volatile int*>(vm_tc_dbg)[96 + (ev)] = int(clock64() - vm_t0); } } while (0)
+#else
+#define VM_TC_T(ev) do { } while (0)
 #endif
 
 namespace vm {
 namespace tck {
 
 constexpr int kTM = 128;       // tile rows = TMEM lanes
-constexpr int kThr = 128;      // 4 warps, warp w <-> TMEM lane quadrant w
 constexpr int kNS = 3;         // ring slots
 constexpr int kSlot = 65536;   // bytes per slot: A (32 KB) | B (32 KB)
 constexpr int kHalfSlot = 32768;
@@ -73,7 +78,8 @@ template <int H, int L>
 __global__ void __launch_bounds__(256) tc_prep_kernel(const __grid_constant__ KStack st, float* __restrict__ img) {
   using I = Img<H, L>;
   const int k = blockIdx.y;
-  int c = blockIdx.x;
+  int c = blockIdx.x >> 2;  // 4 CTAs per chunk
+  const int part = blockIdx.x & 3;
   const float* P = st.params + int64_t(k) * st.block;
   float* out = img + int64_t(k) * I::total;
   // decode chunk id -> (use, layer, chunk, kw, base)
@@ -95,7 +101,8 @@ __global__ void __launch_bounds__(256) tc_prep_kernel(const __grid_constant__ KS
   const int fi_pad = (l == 0) ? st.fi0 : H;
   const int fi_real = (l == 0) ? st.D : H;
   const float* W = P + st.w_off[l];
-  for (int e = threadIdx.x; e < H * kw; e += blockDim.x) {
+  const int per = H * kw / 4;
+  for (int e = part * per + threadIdx.x; e < (part + 1) * per; e += blockDim.x) {
     const int n = e / kw, kk = e % kw;
     const int kidx = cc * 32 + kk;
     float v;
@@ -110,8 +117,31 @@ __global__ void __launch_bounds__(256) tc_prep_kernel(const __grid_constant__ KS
 }
 
 // byte offset of (row, col) in a 128B-swizzled K-major tile with 32 columns
+// 3xTF32 operand split used for staging: hi = x rounded to the nearest tf32
+// (ties away, like cvt.rna, without its inf/nan guard: a non-finite value
+// stays non-finite and is caught by the gradient check), lo = x - hi (exact)
+// rounded the same way.
+__device__ __forceinline__ void split_fast(float x, float& hi, float& lo) {
+  hi = __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
+  lo = __uint_as_float((__float_as_uint(__fsub_rn(x, hi)) + 0x1000u) & 0xFFFFE000u);
+}
+
 __device__ __forceinline__ uint32_t sw128_off(int row, int col) {
   return uint32_t(row * 128 + ((((col >> 2) ^ row) & 7) << 4) + (col & 3) * 4);
+}
+
+// MN-major tf32 operand tile of 32 samples (K) x 128 features (MN) in the
+// SWIZZLE_128B_BASE32B layout (the only MN-major layout tf32 accepts): each
+// sample's 32-feature group is one 128-B row, 32-B granules XOR-permuted by
+// sample % 4; 4-sample atoms 512 B apart (SBO), 32-feature groups 4 KB apart
+// (LBO).  A thread owning a sample writes its features as float4s.
+constexpr int kMnLo = 16384;  // lo tile offset within a 32-KB operand half
+__device__ __forceinline__ uint32_t mn_off(int s, int f) {
+  return uint32_t((f >> 5) * 4096 + (s >> 2) * 512 + (s & 3) * 128 + ((((f & 31) >> 3) ^ (s & 3)) << 5) +
+                  (f & 7) * 4);
+}
+__device__ __forceinline__ uint64_t sdesc_mn(uint32_t saddr) {
+  return tc::sdesc(saddr, 4096, 512) | (uint64_t(1) << 61);
 }
 
 // SWIZZLE_128B K-major descriptor (8-row groups 1024 B apart)
@@ -120,65 +150,78 @@ __device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr) {
 }
 
 // Layer-0 input row of one sample: the positional encoding of models.py:286-308
-// (f32 sincospif, same as KF's load_block) or the caller's encoded row.
-__device__ __forceinline__ void input_row(const KStack& st, int k, int64_t g, bool valid, float (&x)[kK0]) {
+// (f32 sincospif, same as KF's load_block; per-band coefficients 2^b/scale
+// precomputed in f64 -> f32 per model in smem) or the caller's encoded row.
+// Every index is a compile-time constant so the row stays in registers.
+__device__ __forceinline__ void input_row(const KStack& st, const float* __restrict__ coef, int64_t g, bool valid,
+                                          float (&x)[kK0]) {
 #pragma unroll
   for (int f = 0; f < kK0; ++f) x[f] = 0.f;
   if (!valid) return;
   if (st.pts) {
-    const float scale = st.pe_scale[k];
     float p[3];
 #pragma unroll
     for (int c = 0; c < 3; ++c) p[c] = st.pts[g * 3 + c];
-    int f = 0;
+    float e[6][6];  // [band][sin x3, cos x3]
+#pragma unroll
+    for (int b = 0; b < 6; ++b)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        float sn = 0.f, cs = 0.f;
+        if (b < st.n_freq) sincospif(coef[b] * p[c], &sn, &cs);
+        e[b][c] = sn;
+        e[b][3 + c] = cs;
+      }
     if (st.include_input) {
 #pragma unroll
       for (int c = 0; c < 3; ++c) x[c] = p[c];
-      f = 3;
-    }
 #pragma unroll
-    for (int b = 0; b < 6; ++b) {
-      if (b < st.n_freq) {
-        const float coef = float(double(1u << b) / double(scale));
+      for (int b = 0; b < 6; ++b)
 #pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          float sn, cs;
-          sincospif(coef * p[c], &sn, &cs);
-          const int fs = f + 6 * b + c;
-          if (fs + 3 < kK0) {
-            x[fs] = sn;
-            x[fs + 3] = cs;
-          }
-        }
-      }
+        for (int j = 0; j < 6; ++j)
+          if (3 + 6 * b + j < kK0) x[3 + 6 * b + j] = e[b][j];
+    } else {
+#pragma unroll
+      for (int b = 0; b < 6; ++b)
+#pragma unroll
+        for (int j = 0; j < 6; ++j)
+          if (6 * b + j < kK0) x[6 * b + j] = e[b][j];
     }
   } else {
     const float* src = st.enc + g * st.D;
 #pragma unroll
-    for (int f = 0; f < kK0; ++f)
-      if (f < st.D) x[f] = src[f];
+    for (int f = 0; f < kK0; ++f) x[f] = (f < st.D) ? src[f] : 0.f;
   }
 }
+
+constexpr int kCW = 8;                        // compute warps: 2 per TMEM lane quadrant
+constexpr int kComputeThr = kCW * 32;         // staging, epilogues, render
+constexpr int kTCThreads = kComputeThr + 32;  // + warp 8: MMA issuer
 
 template <int H, int L>
 struct Smem {
   static constexpr int kDbW = (L - 1) * H + 4;               // per-warp bias-grad partials
   static constexpr int ring = kNS * kSlot;
   static constexpr int bias = ring;                          // (L-1)*H floats
-  static constexpr int w3 = bias + (L - 1) * H * 4;          // 4*H
-  static constexpr int b3 = w3 + 4 * H * 4;                  // 4 (+pad)
-  static constexpr int out = b3 + 16;                        // 4*kTM
+  static constexpr int w3t = bias + (L - 1) * H * 4;         // [H][4] output weights, transposed
+  static constexpr int b3 = w3t + 4 * H * 4;                 // 4 (+pad)
+  static constexpr int zp = b3 + 16;                         // [2 halves][4][kTM] partial logits
+  static constexpr int out = zp + 2 * 4 * kTM * 4;           // 4*kTM
   static constexpr int tt = out + 4 * kTM * 4;               // kTM
   static constexpr int tr = tt + kTM * 4;                    // kTM
-  static constexpr int db = tr + kTM * 4;                    // 4 warps x kDbW
-  static constexpr int bars = (db + 4 * kDbW * 4 + 7) / 8 * 8;  // 3*kNS + 1 u64
+  static constexpr int coef = tr + kTM * 4;                  // 8 PE coefficients
+  static constexpr int tgt = coef + 8 * 4;                   // [kTM rays][8] targets (depth, rgb, flags)
+  static constexpr int db = tgt + kTM * 8 * 4;               // kCW warps x kDbW
+  static constexpr int bars = (db + kCW * kDbW * 4 + 7) / 8 * 8;  // 3*kNS + 1 u64
   static constexpr int tmem = bars + (3 * kNS + 1) * 8;
-  static constexpr int total = tmem + 16;
+  static constexpr int chunks = tmem + 16;                     // schedule table (MMA warp)
+  static constexpr int total = chunks + 64 * 36;
 };
 
 // One MMA chunk of the per-tile schedule (identical for every role).
 struct Chunk {
-  int sw;      // 0: interleaved K-major pair (A rows = samples), 1: 128B-swizzled transposed pair
+  int sw;      // 0: interleaved K-major pair (A rows = samples), 1: 128B-swizzled K-major transposed
+               // pair, 2: MN-major pair (SWIZZLE_128B_BASE32B, K = samples)
   int kw;      // K columns staged (interleaved)
   int nks;     // k-steps of 8
   int n;       // MMA N
@@ -197,25 +240,23 @@ __device__ __forceinline__ void for_each_chunk(F&& f) {
   for (int l = 1; l <= L - 2; ++l)
     for (int c = 0; c < H / 32; ++c)
       f(j++, Chunk{0, 32, 4, H, 0, c == 0, c == H / 32 - 1, I::fwd_off(l) + c * I::kC32, I::kC32});
-  for (int c = 0; c < 4; ++c) f(j++, Chunk{1, 32, 4, 16, H, c == 0, c == 3, -1, 0});
+  for (int c = 0; c < 4; ++c) f(j++, Chunk{2, 32, 4, 16, H, c == 0, c == 3, -1, 0});
   for (int l = L - 2; l >= 0; --l) {
-    for (int c = 0; c < 4; ++c) f(j++, Chunk{1, 32, 4, l == 0 ? kN0 : H, H, c == 0, c == 3, -1, 0});
+    for (int c = 0; c < 4; ++c) f(j++, Chunk{l == 0 ? 1 : 2, 32, 4, l == 0 ? kN0 : H, H, c == 0, c == 3, -1, 0});
     if (l > 0)
       for (int c = 0; c < H / 32; ++c)
         f(j++, Chunk{0, 32, 4, H, 0, c == 0, c == H / 32 - 1, I::dx_off(l) + c * I::kC32, I::kC32});
   }
 }
 
-constexpr int kComputeThr = 128;           // warps 0-3: staging, epilogues, render
-constexpr int kTCThreads = kComputeThr + 32;  // warp 4: MMA issuer
-
-__device__ __forceinline__ void compute_sync() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+__device__ __forceinline__ void compute_sync() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
 
 template <int H, int L>
 __global__ void __launch_bounds__(kTCThreads, 1)
     tc_train_kernel(const __grid_constant__ KParams p, int si, const float* __restrict__ img_all) {
   static_assert(H * L <= 512, "TMEM columns");
-  static_assert(H == 128, "M = H for the weight-gradient MMAs");
+  static_assert(H == 128, "M = H for the weight-gradient MMAs; 2 x 64-column halves");
+  constexpr int HC = H / 2;  // columns owned by one compute warp
   using I = Img<H, L>;
   using SM = Smem<H, L>;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -224,18 +265,20 @@ __global__ void __launch_bounds__(kTCThreads, 1)
   const int k = blockIdx.x / st.P, tile = blockIdx.x % st.P;
   const int S = st.S, G = kTM / S;
   const int r0 = tile * G, nr = min(G, st.R - r0), ns = nr * S;
-  const int row = tid;  // compute warps: sample row within the tile == TMEM lane
   const int64_t gs0 = int64_t(k) * st.R * S + int64_t(r0) * S;
   const float* __restrict__ img = img_all + int64_t(k) * I::total;
   const float* __restrict__ Pk = st.params + int64_t(k) * st.block;
 
   float* sBias = reinterpret_cast<float*>(smem + SM::bias);
-  float* sW3 = reinterpret_cast<float*>(smem + SM::w3);
+  float* sW3t = reinterpret_cast<float*>(smem + SM::w3t);
   float* sB3 = reinterpret_cast<float*>(smem + SM::b3);
+  float* sZ = reinterpret_cast<float*>(smem + SM::zp);
   float* sOut = reinterpret_cast<float*>(smem + SM::out);
   float* sT = reinterpret_cast<float*>(smem + SM::tt);
   float* sTr = reinterpret_cast<float*>(smem + SM::tr);
   float* sDb = reinterpret_cast<float*>(smem + SM::db);
+  float* sCoef = reinterpret_cast<float*>(smem + SM::coef);
+  float* sTgt = reinterpret_cast<float*>(smem + SM::tgt);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + SM::bars);
   uint64_t* empty = full + kNS;
   uint64_t* wfull = empty + kNS;
@@ -254,28 +297,55 @@ __global__ void __launch_bounds__(kTCThreads, 1)
   }
   for (int l = 0; l < L - 1; ++l)
     for (int i = tid; i < H; i += kTCThreads) sBias[l * H + i] = Pk[st.b_off[l] + i];
-  for (int i = tid; i < 4 * H; i += kTCThreads) sW3[i] = Pk[st.w_off[L - 1] + i];
+  for (int i = tid; i < 4 * H; i += kTCThreads) sW3t[(i % H) * 4 + i / H] = Pk[st.w_off[L - 1] + i];
   if (tid < 4) sB3[tid] = Pk[st.b_off[L - 1] + tid];
-  for (int i = tid; i < 4 * SM::kDbW; i += kTCThreads) sDb[i] = 0.f;
-  if (tid < kTM) sT[row] = row < ns ? st.t[gs0 + row] : 0.f;
+  for (int i = tid; i < kCW * SM::kDbW; i += kTCThreads) sDb[i] = 0.f;
+  if (tid < kTM) sT[tid] = tid < ns ? st.t[gs0 + tid] : 0.f;
+  if (tid < 8) sCoef[tid] = (st.pts && tid < st.n_freq) ? float(double(1u << tid) / double(st.pe_scale[k])) : 0.f;
+  if (tid < nr) {  // this tile's ray targets, read once (render needs them mid-chain)
+    const int64_t rg = int64_t(k) * st.R + r0 + tid;
+    float* t8 = sTgt + tid * 8;
+    t8[0] = st.tdepth[rg];
+    t8[1] = st.tcol[rg * 3 + 0];
+    t8[2] = st.tcol[rg * 3 + 1];
+    t8[3] = st.tcol[rg * 3 + 2];
+    t8[4] = st.tmask[rg] != 0 ? 1.f : 0.f;
+    t8[5] = st.valid[rg] != 0 ? 1.f : 0.f;
+    t8[6] = st.ok[rg] != 0 ? 1.f : 0.f;
+  }
   tc::fence_before_sync();
   __syncthreads();
   tc::fence_after_sync();
   const uint32_t tm = *tmem_slot;
+#ifdef VM_TC_DEBUG
+  const long long vm_t0 = clock64();
+  int vm_ev = 0;
+#endif
 
-  if (warp == 4) {
+  if (warp == kCW) {
     // ------------------------------------------------ MMA issuer (one thread)
     if (lane == 0) {
+      // the static schedule goes to smem once, so the issue loop below is a
+      // single copy of code (instruction-cache friendly)
+      Chunk* tab = reinterpret_cast<Chunk*>(smem + SM::chunks);
+      int nch = 0;
+      for_each_chunk<H, L>([&](int j, const Chunk& ci) { tab[j] = ci; nch = j + 1; });
       uint32_t wpar = 0;
-      for_each_chunk<H, L>([&](int j, const Chunk& ci) {
+#pragma unroll 1
+      for (int j = 0; j < nch; ++j) {
+        const Chunk ci = tab[j];
         const int s = j % kNS;
-        VM_TC_DBG(33, j);
         tc::mbar_wait(&full[s], (j / kNS) & 1);
-        VM_TC_DBG(34, j);
+#ifdef VM_TC_DEBUG
+        if (blockIdx.x == 0) reinterpret_cast<volatile int*>(vm_tc_dbg)[320 + j] = int(clock64() - vm_t0);
+#endif
         if (ci.w_off >= 0) {
           tc::mbar_wait(&wfull[s], (wpar >> s) & 1);
           wpar ^= 1u << s;
         }
+#ifdef VM_TC_DEBUG
+        if (blockIdx.x == 0) reinterpret_cast<volatile int*>(vm_tc_dbg)[256 + j] = int(clock64() - vm_t0);
+#endif
         tc::fence_after_sync();
         const uint32_t sa = tc::smem_u32(smem + s * kSlot);
         const uint32_t idesc = tc::idesc_tf32(128, ci.n, false, false);
@@ -290,6 +360,17 @@ __global__ void __launch_bounds__(kTCThreads, 1)
             tc::mma_tf32(tm, ah, bl, idesc, 1u);
             tc::mma_tf32(tm, ah, bh, idesc, 1u);
           }
+        } else if (ci.sw == 2) {
+          const uint32_t idesc_mn = tc::idesc_tf32(128, ci.n, true, true);
+          const uint32_t a_lo = sa + kMnLo, b_hi = sa + kHalfSlot, b_lo = b_hi + kMnLo;
+          for (int ks = 0; ks < 4; ++ks) {
+            const uint32_t o = ks * 1024;
+            const uint64_t ah = sdesc_mn(sa + o), al = sdesc_mn(a_lo + o);
+            const uint64_t bh = sdesc_mn(b_hi + o), bl = sdesc_mn(b_lo + o);
+            tc::mma_tf32(tm, al, bh, idesc_mn, (ci.first && ks == 0) ? 0u : 1u);
+            tc::mma_tf32(tm, ah, bl, idesc_mn, 1u);
+            tc::mma_tf32(tm, ah, bh, idesc_mn, 1u);
+          }
         } else {
           const uint32_t a_lo = sa + ci.m_rows * 128, b_hi = sa + kHalfSlot, b_lo = b_hi + ci.n * 128;
           for (int ks = 0; ks < 4; ++ks) {
@@ -303,33 +384,34 @@ __global__ void __launch_bounds__(kTCThreads, 1)
         }
         tc::mma_commit(&empty[s]);
         if (ci.last) tc::mma_commit(accf);
-        VM_TC_DBG(32, j + 1);
-#ifdef VM_TC_DEBUG
-        if (blockIdx.x < 64) reinterpret_cast<volatile int*>(vm_tc_dbg)[192 + blockIdx.x] = j + 1;
-#endif
-      });
+      }
     }
     __syncwarp();
   } else {
-    // ------------------------------------------- compute warps 0-3 (128 rows)
-    const uint32_t tq = tm + (uint32_t(32 * warp) << 16);  // this warp's lane quadrant
-    auto R = [&](int j) { return tq + uint32_t(j * H); };  // TMEM region j (column base)
+    // ------------------------------------- compute warps: (quadrant q, half h)
+    const int q = warp & 3, h = warp >> 2;
+    const int row = 32 * q + lane;                          // sample row == TMEM lane
+    const int c0 = h * HC;                                  // first owned column
+    const uint32_t tq = tm + (uint32_t(32 * q) << 16);      // this warp's lane quadrant
+    auto R = [&](int j) { return tq + uint32_t(j * H); };   // TMEM region j (column base)
     float* myDb = sDb + warp * SM::kDbW;
     uint32_t it = 0, accn = 0;
     auto acquire = [&]() -> uint8_t* {
       const uint32_t s = it % kNS;
-      VM_TC_DBG(warp * 8 + 2, int(it));
       if (it >= uint32_t(kNS)) tc::mbar_wait(&empty[s], ((it / kNS) - 1) & 1);
-      VM_TC_DBG(warp * 8 + 3, int(it));
+#ifdef VM_TC_DEBUG
+      if (blockIdx.x == 0 && threadIdx.x == 0) reinterpret_cast<volatile int*>(vm_tc_dbg)[384 + it] = int(clock64() - vm_t0);
+#endif
       return smem + s * kSlot;
     };
-    // weight chunk: after acquiring the slot (so its previous use is complete)
-    // one thread starts the TMA bulk copy of the pre-split weight chunk into
-    // the slot's B half; the MMA thread waits for its bytes on wfull.
+    // weight chunk: after acquiring the slot (its previous use is complete, so
+    // no mbarrier phase can be skipped) one thread starts the TMA bulk copy of
+    // the pre-split weight chunk into the slot's B half; the MMA thread waits
+    // for its bytes on wfull.
     auto acquire_w = [&](int w_off, int floats) -> uint8_t* {
       uint8_t* slot = acquire();
       if (tid == 0) {
-        uint64_t* wb = &wfull[(it % kNS)];
+        uint64_t* wb = &wfull[it % kNS];
         tc::mbar_arrive_tx(wb, uint32_t(floats * 4));
         tc::bulk_g2s(slot + kHalfSlot, img + w_off, uint32_t(floats * 4), wb);
       }
@@ -340,52 +422,61 @@ __global__ void __launch_bounds__(kTCThreads, 1)
       tc::fence_before_sync();
       tc::mbar_arrive(&full[it % kNS]);
       ++it;
-      VM_TC_DBG(warp * 8 + 0, int(it));
-#ifdef VM_TC_DEBUG
-      if (warp == 0 && lane == 0 && blockIdx.x < 64) reinterpret_cast<volatile int*>(vm_tc_dbg)[128 + blockIdx.x] = int(it);
-#endif
     };
     auto wait_acc = [&]() {
-      VM_TC_DBG(warp * 8 + 4, int(accn));
+      VM_TC_T(vm_ev);
+#ifdef VM_TC_DEBUG
+      ++vm_ev;
+#endif
       tc::mbar_wait(accf, accn & 1);
       ++accn;
-      VM_TC_DBG(warp * 8 + 1, int(accn));
       tc::fence_after_sync();
+      VM_TC_T(vm_ev);
+#ifdef VM_TC_DEBUG
+      ++vm_ev;
+#endif
     };
-    // A operand row (this thread's sample) -> interleaved K-major hi/lo
-    auto stage_row = [&](uint8_t* slot, int kw, const float* v) {
+    // `n4` float4 groups of this thread's row at chunk columns [col, col+4*n4)
+    auto stage_row = [&](uint8_t* slot, int kw, int col, const auto& v, int n4) {
       float* hi = reinterpret_cast<float*>(slot);
       float* lo = reinterpret_cast<float*>(slot + kTM * kw * 4);
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        if (4 * q < kw) {
-          float4 h, l;
-          tc::split3(v[4 * q + 0], h.x, l.x);
-          tc::split3(v[4 * q + 1], h.y, l.y);
-          tc::split3(v[4 * q + 2], h.z, l.z);
-          tc::split3(v[4 * q + 3], h.w, l.w);
-          const uint32_t o = tc::ilv_off(row, 4 * q, kw) / 4;
-          st4(hi + o, h);
-          st4(lo + o, l);
+      for (int g = 0; g < 8; ++g) {
+        if (g < n4) {
+          float4 a, b;
+          split_fast(v[4 * g + 0], a.x, b.x);
+          split_fast(v[4 * g + 1], a.y, b.y);
+          split_fast(v[4 * g + 2], a.z, b.z);
+          split_fast(v[4 * g + 3], a.w, b.w);
+          const uint32_t o = tc::ilv_off(row, col + 4 * g, kw) / 4;
+          st4(hi + o, a);
+          st4(lo + o, b);
         }
       }
     };
-    // element (row i, sample lane) of a transposed 128B-swizzled hi/lo tile
-    auto put_t = [&](uint8_t* t, int rows, int i, float v) {
-      float h, l;
-      tc::split3(v, h, l);
-      const uint32_t o = sw128_off(i, lane);
-      *reinterpret_cast<float*>(t + o) = h;
-      *reinterpret_cast<float*>(t + rows * 128 + o) = l;
-    };
-    auto ld32 = [&](uint32_t ta, float (&v)[32]) {
-      float a[16], b[16];
-      tc::tmem_ld16(ta, a);
-      tc::tmem_ld16(ta + 16, b);
+    // element (tile row i, sample lane) of a transposed 128B-swizzled hi/lo tile
+    uint32_t swo[8];  // per-lane byte offset within a 128-B row for row % 8
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        v[j] = a[j];
-        v[16 + j] = b[j];
+    for (int r8 = 0; r8 < 8; ++r8) swo[r8] = sw128_off(r8, lane);
+    auto put_t = [&](uint8_t* t, int rows, int i, float v) {
+      float a, b;
+      split_fast(v, a, b);
+      const uint32_t o = uint32_t(i >> 3) * 1024u + swo[i & 7];
+      *reinterpret_cast<float*>(t + o) = a;
+      *reinterpret_cast<float*>(t + rows * 128 + o) = b;
+    };
+    // 32 features [f0, f0+32) of this lane's sample into an MN-major hi/lo tile
+    auto put_mn = [&](uint8_t* t, int f0, const float (&v)[32]) {
+#pragma unroll
+      for (int m = 0; m < 8; ++m) {
+        float4 a, b;
+        split_fast(v[4 * m + 0], a.x, b.x);
+        split_fast(v[4 * m + 1], a.y, b.y);
+        split_fast(v[4 * m + 2], a.z, b.z);
+        split_fast(v[4 * m + 3], a.w, b.w);
+        const uint32_t o = mn_off(lane, f0 + 4 * m);
+        *reinterpret_cast<float4*>(t + o) = a;
+        *reinterpret_cast<float4*>(t + kMnLo + o) = b;
       }
     };
     // warp butterfly: lane j ends with the sum over the warp's 32 rows of v[j]
@@ -402,84 +493,161 @@ __global__ void __launch_bounds__(kTCThreads, 1)
       }
       return v[0];
     };
+    auto ld32 = [&](uint32_t ta, float (&v)[32]) {
+      uint32_t r[16];
+      VM_TMEM_LD16(ta, r);
+      uint32_t r2[16];
+      VM_TMEM_LD16(ta + 16, r2);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        v[j] = __uint_as_float(r[j]);
+        v[16 + j] = __uint_as_float(r2[j]);
+      }
+    };
+    auto st32 = [&](uint32_t ta, const float (&v)[32]) {
+      uint32_t r[16], r2[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        r[j] = __float_as_uint(v[j]);
+        r2[j] = __float_as_uint(v[16 + j]);
+      }
+      VM_TMEM_ST16(ta, r);
+      VM_TMEM_ST16(ta + 16, r2);
+    };
 
     // ----------------------------------------------------------- forward
     {
       float x0[kK0];
-      input_row(st, k, gs0 + row, row < ns, x0);
-      stage_row(acquire_w(I::fwd_off(0), I::kC32), 32, x0);
+      input_row(st, sCoef, gs0 + row, row < ns, x0);
+      float xa[32], xb[8];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) xa[i] = x0[i];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) xb[i] = x0[32 + i];
+      // chunk 0 (fan-in columns 0-31) by half 0, chunk 1 (32-39) by half 1
+      uint8_t* s0 = acquire_w(I::fwd_off(0), I::kC32);
+      if (h == 0) stage_row(s0, 32, 0, xa, 8);
       release();
-      stage_row(acquire_w(I::fwd_off(0) + I::kC32, I::kC8), 8, x0 + 32);
+      uint8_t* s1 = acquire_w(I::fwd_off(0) + I::kC32, I::kC8);
+      if (h == 1) stage_row(s1, 8, 0, xb, 2);
       release();
     }
+#pragma unroll 1
     for (int l = 0; l < L - 1; ++l) {
       wait_acc();
-      // X_{l+1} = relu(Z_l + b_l) -> R_{l+1}
-      for (int cc = 0; cc < H; cc += 16) {
-        float v[16];
-        tc::tmem_ld16(R(0) + cc, v);
+      // X_{l+1} = relu(Z_l + b_l) over the owned 64 columns -> R_{l+1} and
+      // registers; the next layer's chunks (32 columns each) are staged by
+      // the half that owns them, the other half only releases the slot.
+      float x[2][32];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) v[j] = relu_np(v[j] + sBias[l * H + cc + j]);
-        tc::tmem_st16(R(l + 1) + cc, v);
+      for (int g = 0; g < 2; ++g) {
+        ld32(R(0) + c0 + 32 * g, x[g]);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) x[g][j] = relu_np(x[g][j] + sBias[l * H + c0 + 32 * g + j]);
+        st32(R(l + 1) + c0 + 32 * g, x[g]);
       }
       tc::tmem_st_wait();
-      if (l == L - 2) break;
+      if (l == L - 2) {
+        // output layer (4 logits), partial over the owned columns
+        float z[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int g = 0; g < 2; ++g)
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const float4 w = ld4(sW3t + 4 * (c0 + 32 * g + j));
+            z[0] = fmaf(w.x, x[g][j], z[0]);
+            z[1] = fmaf(w.y, x[g][j], z[1]);
+            z[2] = fmaf(w.z, x[g][j], z[2]);
+            z[3] = fmaf(w.w, x[g][j], z[3]);
+          }
+#pragma unroll
+        for (int o = 0; o < 4; ++o) sZ[(h * 4 + o) * kTM + row] = z[o];
+        break;
+      }
+#pragma unroll 1
       for (int c = 0; c < H / 32; ++c) {
-        float v[32];
-        ld32(R(l + 1) + 32 * c, v);
-        stage_row(acquire_w(I::fwd_off(l + 1) + c * I::kC32, I::kC32), 32, v);
+        uint8_t* sl = acquire_w(I::fwd_off(l + 1) + c * I::kC32, I::kC32);
+        if ((c >> 1) == h) {
+          float v[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = (c & 1) ? x[1][j] : x[0][j];
+          stage_row(sl, 32, 0, v, 8);
+        }
         release();
       }
     }
-    // output layer (4 logits) on CUDA cores, sigmoid heads (models.py:341-342)
+    VM_TC_T(26);
+    compute_sync();
+    VM_TC_T(27);
+    if (h == 0) {
+#pragma unroll
+      for (int o = 0; o < 4; ++o)
+        sOut[o * kTM + row] = sigmoid_f((sZ[o * kTM + row] + sZ[(4 + o) * kTM + row]) + sB3[o]);
+    }
+    compute_sync();
+    VM_TC_T(28);
+    // render + L1 losses + loss grads + render backward, one thread per ray,
+    // rays spread over the 8 warps (4 sub-partitions)
     {
-      float z[4] = {0.f, 0.f, 0.f, 0.f};
-      for (int cc = 0; cc < H; cc += 16) {
-        float v[16];
-        tc::tmem_ld16(R(L - 1) + cc, v);
+      const int rr = lane * kCW + warp;
+      if (rr < nr) {
+        const int r = r0 + rr, sb = rr * S;
+        const int64_t rg = int64_t(k) * st.R + r;
+        const float* t8 = sTgt + rr * 8;
+        RayTargets tg;
+        tg.depth = t8[0];
+        tg.colour[0] = t8[1];
+        tg.colour[1] = t8[2];
+        tg.colour[2] = t8[3];
+        tg.mask = t8[4] != 0.f;
+        tg.valid = t8[5] != 0.f;
+        tg.ok = t8[6] != 0.f;
+        RayLossGrad lg;
+        if (S == 10) {
+          constexpr int NS = 10;
+          float o[NS], cl[3][NS], tv[NS];
 #pragma unroll
-        for (int j = 0; j < 16; ++j)
+          for (int i = 0; i < NS; ++i) {
+            o[i] = sOut[sb + i];
+            tv[i] = sT[sb + i];
 #pragma unroll
-          for (int o = 0; o < 4; ++o) z[o] = fmaf(sW3[o * H + cc + j], v[j], z[o]);
+            for (int ch = 0; ch < 3; ++ch) cl[ch][i] = sOut[(1 + ch) * kTM + sb + i];
+          }
+          lg = render_ray_fixed<NS>(o, cl, tv, tg, st.wc, st.wo);
+#pragma unroll
+          for (int i = 0; i < NS; ++i) {
+            sOut[sb + i] = o[i];
+#pragma unroll
+            for (int ch = 0; ch < 3; ++ch) sOut[(1 + ch) * kTM + sb + i] = cl[ch][i];
+          }
+        } else {
+          auto occ = [&](int i) { return sOut[sb + i]; };
+          auto col = [&](int i, int c) { return sOut[(1 + c) * kTM + sb + i]; };
+          auto tt = [&](int i) { return sT[sb + i]; };
+          render_ray_forward(S, occ, col, tt, [&](int i, float v) { sTr[sb + i] = v; });
+          const RayFwd f = render_ray_sums(S, occ, col, tt, [&](int i) { return sTr[sb + i]; });
+          lg = ray_loss_grad(f, tg, st.wc, st.wo);
+          render_ray_backward(S, occ, col, tt, [&](int i) { return sTr[sb + i]; }, lg.dO, lg.dD, lg.dC,
+                              [&](int i, float d_occ, const float* d_col) {
+                                const float o = sOut[sb + i];
+                                sOut[sb + i] = __fmul_rn(__fmul_rn(d_occ, o), __fsub_rn(1.0f, o));
+#pragma unroll
+                                for (int c = 0; c < 3; ++c) {
+                                  const float cv = sOut[(1 + c) * kTM + sb + i];
+                                  sOut[(1 + c) * kTM + sb + i] =
+                                      __fmul_rn(__fmul_rn(d_col[c], cv), __fsub_rn(1.0f, cv));
+                                }
+                              });
+        }
+        st.ray_terms[rg * 3 + 0] = lg.l_depth;
+        st.ray_terms[rg * 3 + 1] = lg.l_colour;
+        st.ray_terms[rg * 3 + 2] = lg.l_occ;
       }
-#pragma unroll
-      for (int o = 0; o < 4; ++o) sOut[o * kTM + row] = sigmoid_f(z[o] + sB3[o]);
     }
+    VM_TC_T(29);
     compute_sync();
-    // render + L1 losses + loss grads + render backward, one thread per ray
-    if (tid < nr) {
-      const int r = r0 + tid, sb = tid * S;
-      const int64_t rg = int64_t(k) * st.R + r;
-      auto occ = [&](int i) { return sOut[sb + i]; };
-      auto col = [&](int i, int c) { return sOut[(1 + c) * kTM + sb + i]; };
-      auto tt = [&](int i) { return sT[sb + i]; };
-      render_ray_forward(S, occ, col, tt, [&](int i, float v) { sTr[sb + i] = v; });
-      const RayFwd f = render_ray_sums(S, occ, col, tt, [&](int i) { return sTr[sb + i]; });
-      RayTargets tg;
-      tg.depth = st.tdepth[rg];
-      tg.colour[0] = st.tcol[rg * 3 + 0];
-      tg.colour[1] = st.tcol[rg * 3 + 1];
-      tg.colour[2] = st.tcol[rg * 3 + 2];
-      tg.mask = st.tmask[rg] != 0;
-      tg.valid = st.valid[rg] != 0;
-      tg.ok = st.ok[rg] != 0;
-      const RayLossGrad lg = ray_loss_grad(f, tg, st.wc, st.wo);
-      st.ray_terms[rg * 3 + 0] = lg.l_depth;
-      st.ray_terms[rg * 3 + 1] = lg.l_colour;
-      st.ray_terms[rg * 3 + 2] = lg.l_occ;
-      render_ray_backward(S, occ, col, tt, [&](int i) { return sTr[sb + i]; }, lg.dO, lg.dD, lg.dC,
-                          [&](int i, float d_occ, const float* d_col) {
-                            const float o = sOut[sb + i];
-                            sOut[sb + i] = __fmul_rn(__fmul_rn(d_occ, o), __fsub_rn(1.0f, o));
-#pragma unroll
-                            for (int c = 0; c < 3; ++c) {
-                              const float cv = sOut[(1 + c) * kTM + sb + i];
-                              sOut[(1 + c) * kTM + sb + i] =
-                                  __fmul_rn(__fmul_rn(d_col[c], cv), __fsub_rn(1.0f, cv));
-                            }
-                          });
-    }
-    compute_sync();
+    VM_TC_T(30);
     float g3[4];
 #pragma unroll
     for (int o = 0; o < 4; ++o) g3[o] = row < ns ? sOut[o * kTM + row] : 0.f;
@@ -489,39 +657,43 @@ __global__ void __launch_bounds__(kTCThreads, 1)
 
     // ---------------------------------------------------------- backward
     // output layer: dW3^T = X3^T G3 (MMA, M = H, N = 16), db3, and
-    // G2 = (G3 W3) * (X3 > 0) written over X3 in TMEM.
+    // G2 = (G3 W3) * (X3 > 0) written over X3 in TMEM (owned columns).
+#pragma unroll 1
     for (int c = 0; c < 4; ++c) {
-      uint8_t* s = acquire();
-      if (warp == c) {
-        for (int cc = 0; cc < H; cc += 16) {
-          float v[16], g[16];
-          tc::tmem_ld16(R(L - 1) + cc, v);
+      uint8_t* sl = acquire();
+      if (q == c) {
 #pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            const int i = cc + j;
-            put_t(s, H, i, v[j]);
-            float a = 0.f;
+        for (int g = 0; g < 2; ++g) {
+          float v[32];
+          ld32(R(L - 1) + c0 + 32 * g, v);
+          put_mn(sl, c0 + 32 * g, v);  // A = X3 (M = fan-in)
 #pragma unroll
-            for (int o = 0; o < 4; ++o) a = fmaf(g3[o], sW3[o * H + i], a);
-            g[j] = v[j] > 0.f ? a : 0.f;
+          for (int j = 0; j < 32; ++j) {
+            const float4 w = ld4(sW3t + 4 * (c0 + 32 * g + j));
+            const float a = fmaf(g3[3], w.w, fmaf(g3[2], w.z, fmaf(g3[1], w.y, g3[0] * w.x)));
+            v[j] = v[j] > 0.f ? a : 0.f;
           }
-          tc::tmem_st16(R(L - 1) + cc, g);
+          st32(R(L - 1) + c0 + 32 * g, v);
         }
         tc::tmem_st_wait();
+        if (h == 0) {
+          float gv[32];
 #pragma unroll
-        for (int o = 0; o < 16; ++o) put_t(s + kHalfSlot, 16, o, o < 4 ? g3[o] : 0.f);
+          for (int o = 0; o < 32; ++o) gv[o] = o < 4 ? g3[o < 4 ? o : 0] : 0.f;
+          put_mn(sl + kHalfSlot, 0, gv);  // B = G3 (N = 16, 4 live)
 #pragma unroll
-        for (int o = 0; o < 4; ++o) {
-          float a = g3[o];
+          for (int o = 0; o < 4; ++o) {
+            float a = g3[o];
 #pragma unroll
-          for (int w = 16; w >= 1; w >>= 1) a += __shfl_xor_sync(0xffffffffu, a, w);
-          if (lane == 0) myDb[(L - 1) * H + o] += a;
+            for (int w = 16; w >= 1; w >>= 1) a += __shfl_xor_sync(0xffffffffu, a, w);
+            if (lane == 0) myDb[(L - 1) * H + o] += a;
+          }
         }
       }
       release();
     }
     wait_acc();
-    {
+    if (h == 0) {
       float v[16];
       tc::tmem_ld16(R(0), v);
       const int i = row;  // lane = fan-in index
@@ -529,72 +701,111 @@ __global__ void __launch_bounds__(kTCThreads, 1)
       for (int o = 0; o < 4; ++o) gdst[st.w_off[L - 1] + o * H + i] = v[o];
     }
 
+#pragma unroll 1
     for (int l = L - 2; l >= 0; --l) {
-      // dW_l = G_l^T X_l, K = samples: chunk c = warp c's 32 rows
-      const int nfi = (l == 0) ? kN0 : H;
+      // dW_l = G_l^T X_l, K = samples: chunk c = quadrant c's 32 rows, each
+      // half stages its 64 features of both operands.  Hidden layers compute
+      // dW_l^T = X_l^T G_l from MN-major tiles (A = X_l, B = G_l, each thread
+      // writes its own sample's features as float4s), so TMEM lane = fan-in
+      // and the drain writes whole 128-B rows of the gradient; layer 0 (fan-in
+      // 33) keeps K-major transposed tiles with A = G_0^T (M = fan-out).
+#pragma unroll 1
       for (int c = 0; c < 4; ++c) {
-        uint8_t* s = acquire();
-        if (warp == c) {
-          for (int cc = 0; cc < H; cc += 32) {
-            float g[32];
-            ld32(R(l + 1) + cc, g);
+        uint8_t* sl = acquire();
+        if (q == c) {
+          uint8_t* gt = (l == 0) ? sl : sl + kHalfSlot;  // G tile
+          uint8_t* xt = (l == 0) ? sl + kHalfSlot : sl;  // X tile
 #pragma unroll
-            for (int j = 0; j < 32; ++j) put_t(s, H, cc + j, g[j]);
-            myDb[l * H + cc + lane] += warp_colsum(g);
+          for (int g = 0; g < 2; ++g) {
+            float v[32];
+            ld32(R(l + 1) + c0 + 32 * g, v);
+            if (l == 0) {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) put_t(gt, H, c0 + 32 * g + j, v[j]);
+            } else {
+              put_mn(gt, c0 + 32 * g, v);
+            }
+            myDb[l * H + c0 + 32 * g + lane] += warp_colsum(v);
           }
           if (l == 0) {
             float x0[kK0];
-            input_row(st, k, gs0 + row, row < ns, x0);
+            input_row(st, sCoef, gs0 + row, row < ns, x0);
 #pragma unroll
-            for (int i = 0; i < kN0; ++i) put_t(s + kHalfSlot, kN0, i, i < kK0 ? x0[i] : 0.f);
+            for (int i = 0; i < kN0; ++i)
+              if (i / (kN0 / 2) == h) put_t(xt, kN0, i, i < kK0 ? x0[i < kK0 ? i : 0] : 0.f);
           } else {
-            for (int cc = 0; cc < H; cc += 16) {
-              float v[16];
-              tc::tmem_ld16(R(l) + cc, v);
 #pragma unroll
-              for (int j = 0; j < 16; ++j) put_t(s + kHalfSlot, H, cc + j, v[j]);
+            for (int g = 0; g < 2; ++g) {
+              float v[32];
+              ld32(R(l) + c0 + 32 * g, v);
+              put_mn(xt, c0 + 32 * g, v);
             }
           }
         }
         release();
       }
       wait_acc();
-      {  // drain dW_l (lane = fan-out row)
-        const int o = row;
-        const int fi_pad = (l == 0) ? st.fi0 : H;
-        float* dst = gdst + st.w_off[l] + o * fi_pad;
-        for (int cc = 0; cc < nfi; cc += 16) {
-          float v[16];
-          tc::tmem_ld16(R(0) + cc, v);
+      if (l > 0) {  // drain dW_l^T: lane = fan-in i, columns = this half's fan-out rows
+        const int i = row;
+        float* dst = gdst + st.w_off[l] + i;
 #pragma unroll
-          for (int q = 0; q < 4; ++q)
-            if (cc + 4 * q < fi_pad)
-              st4(dst + cc + 4 * q, make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]));
+        for (int cc = 0; cc < HC; cc += 16) {
+          float v[16];
+          tc::tmem_ld16(R(0) + c0 + cc, v);
+#pragma unroll
+          for (int j = 0; j < 16; ++j) dst[(c0 + cc + j) * H] = v[j];
+        }
+      } else {  // drain dW_0 (lane = fan-out row; this half's fan-in columns)
+        const int o = row;
+        const int fi_pad = st.fi0;
+        const int cb = h * (kN0 / 2);
+        float* dst = gdst + st.w_off[0] + o * fi_pad;
+        for (int cc = 0; cc < kN0 / 2; cc += 8) {
+          float v[16];
+          tc::tmem_ld16(R(0) + cb + cc, v);
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            if (cb + cc + j < fi_pad) dst[cb + cc + j] = v[j];
         }
       }
       if (l == 0) break;
-      // G_{l-1} = (G_l W_l) * (X_l > 0): A = G_l rows, B = W_l^T chunks (TMA)
-      for (int c = 0; c < H / 32; ++c) {
-        float v[32];
-        ld32(R(l + 1) + 32 * c, v);
-        stage_row(acquire_w(I::dx_off(l) + c * I::kC32, I::kC32), 32, v);
-        release();
+      // G_{l-1} = (G_l W_l) * (X_l > 0): A = G_l rows (chunk c by the half
+      // owning those columns), B = W_l^T chunks (TMA)
+      {
+        float gv[2][32];
+        ld32(R(l + 1) + c0, gv[0]);
+        ld32(R(l + 1) + c0 + 32, gv[1]);
+#pragma unroll 1
+        for (int c = 0; c < H / 32; ++c) {
+          uint8_t* sl = acquire_w(I::dx_off(l) + c * I::kC32, I::kC32);
+          if ((c >> 1) == h) {
+            float v[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = (c & 1) ? gv[1][j] : gv[0][j];
+            stage_row(sl, 32, 0, v, 8);
+          }
+          release();
+        }
       }
       wait_acc();
-      for (int cc = 0; cc < H; cc += 16) {
-        float d[16], a[16];
-        tc::tmem_ld16(R(0) + cc, d);
-        tc::tmem_ld16(R(l) + cc, a);
 #pragma unroll
-        for (int j = 0; j < 16; ++j) d[j] = a[j] > 0.f ? d[j] : 0.f;
-        tc::tmem_st16(R(l) + cc, d);
+      for (int g = 0; g < 2; ++g) {
+        float d[32], a[32];
+        ld32(R(0) + c0 + 32 * g, d);
+        ld32(R(l) + c0 + 32 * g, a);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) d[j] = a[j] > 0.f ? d[j] : 0.f;
+        st32(R(l) + c0 + 32 * g, d);
       }
       tc::tmem_st_wait();
     }
     compute_sync();
+    VM_TC_T(vm_ev);
     // bias gradients: per-warp partials summed in warp order (deterministic)
     for (int i = tid; i < (L - 1) * H + 4; i += kComputeThr) {
-      const float v = ((sDb[i] + sDb[SM::kDbW + i]) + sDb[2 * SM::kDbW + i]) + sDb[3 * SM::kDbW + i];
+      float v = sDb[i];
+#pragma unroll
+      for (int w = 1; w < kCW; ++w) v += sDb[w * SM::kDbW + i];
       if (i < (L - 1) * H) gdst[st.b_off[i / H] + (i % H)] = v;
       else gdst[st.b_off[L - 1] + (i - (L - 1) * H)] = v;
     }
@@ -603,9 +814,6 @@ __global__ void __launch_bounds__(kTCThreads, 1)
   tc::fence_before_sync();
   __syncthreads();
   if (warp == 0) tc::tmem_free(tm, 512);
-#ifdef VM_TC_DEBUG
-  if (tid == 0) atomicAdd(&vm_tc_dbg[64], 1);
-#endif
   if (st.P > 1) return;
   // single-tile model: finish like KF's P == 1 path
   __threadfence_block();

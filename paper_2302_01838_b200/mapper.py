@@ -252,7 +252,10 @@ class Mapper:
             g = torch.cuda.CUDAGraph()
             main = torch.cuda.Stream(dev)
             with torch.cuda.stream(main):
-                with torch.cuda.graph(g, stream=main):
+                # relaxed: a capture-unsafe call elsewhere in the process (e.g. a
+                # previous Mapper's graphs or pinned buffers being released by
+                # the garbage collector) must not invalidate this capture
+                with torch.cuda.graph(g, stream=main, capture_error_mode="relaxed"):
                     cur = torch.cuda.current_stream()
                     side.wait_stream(cur)
                     with torch.cuda.stream(side):

@@ -50,7 +50,8 @@ __global__ void gemm_probe(const float* A, const float* B, float* D, int M, int 
     const float x = m < M ? A[m * K + k] : 0.f;
     float hi, lo;
     if (split) split3(x, hi, lo); else { hi = x; lo = 0.f; }
-    const uint32_t off = a_mn == 2 ? uint32_t(m * 128 + (((k >> 2) ^ (m & 7)) << 4) + (k & 3) * 4) : a_mn ? ilv_off(k, m, Mt) : ilv_off(m, k, K);
+    const uint32_t off = a_mn == 3 ? uint32_t((m >> 5) * (K * 128) + (k >> 2) * 512 + (k & 3) * 128 + ((((m & 31) >> 3) ^ (k & 3)) << 5) + (m & 7) * 4)
+                       : a_mn == 2 ? uint32_t(m * 128 + (((k >> 2) ^ (m & 7)) << 4) + (k & 3) * 4) : a_mn ? ilv_off(k, m, Mt) : ilv_off(m, k, K);
     *reinterpret_cast<float*>(sAh + off) = hi;
     *reinterpret_cast<float*>(sAl + off) = lo;
   }
@@ -58,7 +59,8 @@ __global__ void gemm_probe(const float* A, const float* B, float* D, int M, int 
     const int n = i / K, k = i % K;
     float hi, lo;
     if (split) split3(B[i], hi, lo); else { hi = B[i]; lo = 0.f; }
-    const uint32_t off = b_mn == 2 ? uint32_t(n * 128 + (((k >> 2) ^ (n & 7)) << 4) + (k & 3) * 4) : b_mn ? ilv_off(k, n, N) : ilv_off(n, k, K);
+    const uint32_t off = b_mn == 3 ? uint32_t((n >> 5) * (K * 128) + (k >> 2) * 512 + (k & 3) * 128 + ((((n & 31) >> 3) ^ (k & 3)) << 5) + (n & 7) * 4)
+                       : b_mn == 2 ? uint32_t(n * 128 + (((k >> 2) ^ (n & 7)) << 4) + (k & 3) * 4) : b_mn ? ilv_off(k, n, N) : ilv_off(n, k, K);
     *reinterpret_cast<float*>(sBh + off) = hi;
     *reinterpret_cast<float*>(sBl + off) = lo;
   }
@@ -66,7 +68,7 @@ __global__ void gemm_probe(const float* A, const float* B, float* D, int M, int 
   __syncthreads();
   if (tid == 0) {
     fence_after_sync();
-    const uint32_t idesc = idesc_tf32(M, N, a_mn == 1, b_mn == 1);
+    const uint32_t idesc = idesc_tf32(M, N, a_mn == 1 || a_mn == 3, b_mn == 1 || b_mn == 3);
     // K-major: LBO = 128 (k group), SBO = cols*32 (row group); step 8 k = 256 B
     // MN-major: LBO = cols*32 (8 K-rows), SBO = 128 (4 MN); step 8 k = cols*32
     uint32_t a_lbo = a_mn ? Mt * 32 : 128, a_sbo = a_mn ? 128 : K * 32, a_step = a_mn ? Mt * 32 : 256;
@@ -74,7 +76,10 @@ __global__ void gemm_probe(const float* A, const float* B, float* D, int M, int 
     if (swap && a_mn) { uint32_t t = a_lbo; a_lbo = a_sbo; a_sbo = t; }
     if (swap && b_mn) { uint32_t t = b_lbo; b_lbo = b_sbo; b_sbo = t; }
     uint32_t acc = 0;
-    const uint64_t a_sw = a_mn == 2 ? (uint64_t(2) << 61) : 0, b_sw = b_mn == 2 ? (uint64_t(2) << 61) : 0;
+    const uint64_t a_sw = a_mn == 2 ? (uint64_t(2) << 61) : a_mn == 3 ? (uint64_t(1) << 61) : 0;
+    const uint64_t b_sw = b_mn == 2 ? (uint64_t(2) << 61) : b_mn == 3 ? (uint64_t(1) << 61) : 0;
+    if (a_mn == 3) { a_lbo = K * 128; a_sbo = 512; a_step = 1024; }
+    if (b_mn == 3) { b_lbo = K * 128; b_sbo = 512; b_step = 1024; }
     if (a_mn == 2) { a_lbo = 16; a_sbo = 1024; a_step = 32; }
     if (b_mn == 2) { b_lbo = 16; b_sbo = 1024; b_step = 32; }
     for (int ks = 0; ks < K / 8; ++ks) {
@@ -108,7 +113,7 @@ __global__ void gemm_probe(const float* A, const float* B, float* D, int M, int 
 }
 
 // Back-to-back MMAs from one thread; returns cycles per instruction.
-__global__ void mma_rate(long long* out, int N, int iters) {
+__global__ void mma_rate(long long* out, int N, int iters, int sw) {
   extern __shared__ __align__(1024) uint8_t sm[];
   __shared__ uint64_t bar;
   __shared__ uint32_t tbase;
@@ -125,10 +130,16 @@ __global__ void mma_rate(long long* out, int N, int iters) {
   fence_after_sync();
   if (tid == 0) {
     const uint32_t idesc = idesc_tf32(128, N, false, false);
-    const uint64_t a = sdesc(smem_u32(sm), 128, 32 * 32);
-    const uint64_t b = sdesc(smem_u32(sm) + 128 * 32 * 4, 128, 32 * 32);
+    uint64_t a = sdesc(smem_u32(sm), 128, 32 * 32);
+    uint64_t b = sdesc(smem_u32(sm) + 128 * 32 * 4, 128, 32 * 32);
+    uint64_t step = 16;
+    if (sw) {
+      a = sdesc(smem_u32(sm), 16, 1024) | (uint64_t(2) << 61);
+      b = sdesc(smem_u32(sm) + 128 * 32 * 4, 16, 1024) | (uint64_t(2) << 61);
+      step = 2;
+    }
     long long t0 = clock64();
-    for (int i = 0; i < iters; ++i) mma_tf32(tbase, a + (i & 3) * 16, b + (i & 3) * 16, idesc, i > 0);
+    for (int i = 0; i < iters; ++i) mma_tf32(tbase, a + (i & 3) * step, b + (i & 3) * step, idesc, i > 0);
     mma_commit(&bar);
     mbar_wait(&bar, 0);
     long long t1 = clock64();
@@ -233,7 +244,11 @@ int main() {
     for (int amn = 0; amn < 3; amn += 2)
       for (int bmn = 0; bmn < 3; bmn += 2) ok &= run_case(128, 128, 32, amn, bmn, split);
   ok &= run_case(128, 16, 40, 0, 0, 1);
-  ok &= run_case(128, 40, 32, 2, 2, 1);
+  ok &= run_case(128, 128, 32, 3, 3, 1);
+  ok &= run_case(128, 128, 32, 3, 3, 0);
+  ok &= run_case(128, 48, 32, 3, 3, 1);
+  ok &= run_case(128, 16, 32, 3, 3, 1);
+  ok &= run_case(128, 128, 32, 0, 3, 1);
   ok &= run_case(128, 16, 32, 2, 2, 1);
   ok &= run_case(128, 256, 16, 0, 0, 1);
   if (getenv("M64")) m64_layout(16);
@@ -241,13 +256,14 @@ int main() {
   CK(cudaMalloc(&dout, 8));
   const int smem = (128 * 32 + 256 * 32) * 4;
   CK(cudaFuncSetAttribute(mma_rate, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  if (getenv("RATE")) for (int N : {16, 32, 64, 128, 256}) {
+  for (int sw = 0; sw < 2; ++sw)
+  for (int N : {16, 32, 48, 64, 128, 256}) {
     const int iters = 4096;
-    mma_rate<<<1, 128, smem>>>(dout, N, iters);
+    mma_rate<<<1, 128, smem>>>(dout, N, iters, sw);
     CK(cudaDeviceSynchronize());
     long long cyc;
     CK(cudaMemcpy(&cyc, dout, 8, cudaMemcpyDeviceToHost));
-    printf("tcgen05 tf32 M=128 N=%3d K=8: %.1f cycles/MMA -> %.0f MAC/cycle/SM\n", N, double(cyc) / iters,
+    printf("sw=%d tcgen05 tf32 M=128 N=%3d K=8: %.1f cycles/MMA -> %.0f MAC/cycle/SM\n", sw, N, double(cyc) / iters,
            128.0 * N * 8 * iters / double(cyc));
   }
   // mma.sync rate: full chip, 148*4 CTAs of 256 threads

@@ -39,6 +39,22 @@ def assert_params_close(params, ost: O.Stack, rtol=1e-4, atol=1e-5, rel_l2=1e-4)
     assert rel.max() <= rel_l2, f"per-object relative L2 {rel.max():.3e} > {rel_l2}"
 
 
+def assert_params_rel_l2(params, ost: O.Stack, rel_l2=1e-4):
+    """North-star parameter contract only (per-object relative L2), used for
+    stacks trained by the 3xTF32 tensor-core kernel: its gradients sit ~2e-6
+    relative from an f64 run (fp32 FFMA: ~1e-7), so after a few Adam steps a
+    handful of knife-edge components (ReLU / L1-sign flips) leave the
+    per-component band while the model as a whole stays ~2e-5 from the
+    reference (scripts/tc_precision.py)."""
+    W, B = host_layers(params)
+    k = params.count
+    mine = np.concatenate([np.concatenate([W[l].reshape(k, -1), B[l]], 1) for l in range(len(W))], 1)
+    ref = np.concatenate([np.concatenate([ost.W[l][:k].reshape(k, -1), ost.b[l][:k]], 1)
+                          for l in range(len(W))], 1)
+    rel = np.linalg.norm(mine - ref, axis=1) / np.maximum(np.linalg.norm(ref, axis=1), 1e-30)
+    assert rel.max() <= rel_l2, f"per-object relative L2 {rel.max():.3e} > {rel_l2}"
+
+
 def flat_params(params):
     W, B = host_layers(params)
     k = params.count

@@ -21,8 +21,8 @@ from oracle import vobj_oracle as O
 from paper_2302_01838_b200 import LossWeights, ModelArch, init_stacked, set_frozen, train_on_batch
 from paper_2302_01838_b200.trainer import _synthetic_batch, launch_train, train_on_batch_sequential
 
-from .helpers import (assert_as_close_to_truth, assert_params_close, f64_batch, f64_stack, flat_oracle,
-                      flat_params, oracle_arch, to_host_batch)
+from .helpers import (assert_as_close_to_truth, assert_params_close, assert_params_rel_l2, f64_batch, f64_stack,
+                      flat_oracle, flat_params, oracle_arch, to_host_batch)
 
 pytestmark = pytest.mark.gpu
 
@@ -109,4 +109,23 @@ def test_two_stacks_one_launch(cuda):
         np.testing.assert_allclose(l[:6], np.stack(e1, 1), rtol=1e-4, atol=1e-6)
         np.testing.assert_allclose(l[6:], np.stack(e2, 1), rtol=1e-4, atol=1e-6)
     assert_params_close(po, oo)
-    assert_params_close(pb, ob)
+    assert_params_rel_l2(pb, ob)  # h128 background: tensor-core (3xTF32) kernel
+
+
+def test_tensor_core_gradient_accuracy(cuda):
+    """KT (tcgen05 3xTF32) gradient of one step vs an f64 run of the same
+    algorithm, recovered from Adam's first moment (m = (1 - b1) g): measured
+    relative L2 ~2e-6 per layer on a B200; guard at 2e-5."""
+    ab = ModelArch(hidden=128)
+    pb, sb = init_stacked(ab, 1, seed=0, stream=2)
+    ob = f64_stack(O.new_stack(oracle_arch(ab), 1, 0, stream=2))
+    bb = _synthetic_batch(ab, 1, 1200, 10, seed=4)
+    launch_train([(pb, sb, bb)], LossWeights())
+    O.train_on_batch(ob, f64_batch(to_host_batch(bb)))
+    k = 1
+    for l in range(4):
+        g = sb.m_weights[l][:k].cpu().numpy().astype(np.float64)[0]
+        t = ob.mW[l][0]
+        assert np.linalg.norm(g - t) / np.linalg.norm(t) < 2e-5, f"layer {l}"
+        gb = sb.m_biases[l][:k].cpu().numpy().astype(np.float64)[0]
+        assert np.linalg.norm(gb - ob.mb[l][0]) / np.linalg.norm(ob.mb[l][0]) < 2e-5, f"bias {l}"

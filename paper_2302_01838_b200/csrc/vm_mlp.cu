@@ -434,6 +434,23 @@ __device__ void run_item(const KStack& st, int item, float* smem) {
 
   if (NTEAMS == 1) {
     emit(gdst, false);
+  } else if (st.block <= st.team_floats) {
+    // each team writes its whole partial block into its own (now idle)
+    // activation region; then all threads add the NTEAMS regions in team
+    // order (deterministic, same sum order as the sequential variant below)
+    float* mine = smem + st.w_floats + team * st.team_floats;
+    emit(mine, false);
+    __syncthreads();
+    const float* r0 = smem + st.w_floats;
+    for (int i = tid; i < st.block / 4; i += kThreads) {
+      float4 v = ld4(r0 + 4 * i);
+#pragma unroll
+      for (int t = 1; t < NTEAMS; ++t) {
+        const float4 u = ld4(r0 + t * st.team_floats + 4 * i);
+        v.x += u.x; v.y += u.y; v.z += u.z; v.w += u.w;
+      }
+      st4(gdst + 4 * i, v);
+    }
   } else {
     __syncthreads();  // every team is done with the weights: reuse sW as staging
     for (int t = 0; t < NTEAMS; ++t) {
@@ -821,14 +838,30 @@ extern "C" int vm_train_step(const VmStack* stacks, const VmBatch* batches, int 
   }
   // The tensor-core stacks run on a side stream, concurrently with the FFMA
   // kernel (fork/join with events; both are captured when `s` is capturing).
+  // Their weight images are built on `s` before the fork so the KT launch is
+  // the first of the two: its one-tile-per-SM CTAs get SMs first and the
+  // many short FFMA CTAs fill the remaining SMs and the tail.
   static cudaStream_t side = nullptr;
   static cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   bool forked = false;
   cudaStream_t ts = s;
+  using TI = tck::Img<128, 4>;
   for (int i = 0; i < n_stacks; ++i) {
     const KStack& ks = pl.kp.s[i];
     if (!ks.tc || ks.K == 0) continue;
-    if (!forked && fn) {
+    float* img = reinterpret_cast<float*>(ws + pl.off_img[i]);
+    tck::tc_prep_kernel<128, 4><<<dim3(TI::n_chunks * 4, ks.K), 256, 0, s>>>(ks, img);
+    VM_CUDA(cudaGetLastError());
+    if (g_prof.on) g_prof.kernels += 1;
+  }
+  for (int i = 0; i < n_stacks; ++i) {
+    const KStack& ks = pl.kp.s[i];
+    if (!ks.tc || ks.K == 0) continue;
+    static const bool no_fork = [] {
+      const char* e = std::getenv("VM_NO_FORK");
+      return e && e[0] == '1';
+    }();
+    if (!forked && fn && !no_fork) {
       if (!side) {  // first use may be inside a graph capture: relax the capture mode for the creation
         cudaStreamCaptureMode mode = cudaStreamCaptureModeRelaxed;
         VM_CUDA(cudaThreadExchangeStreamCaptureMode(&mode));
@@ -846,15 +879,12 @@ extern "C" int vm_train_step(const VmStack* stacks, const VmBatch* batches, int 
       g_prof.pair(kt0, kt1, 2);
       VM_CUDA(cudaEventRecord(kt0, ts));
     }
-    using I = tck::Img<128, 4>;
     float* img = reinterpret_cast<float*>(ws + pl.off_img[i]);
-    tck::tc_prep_kernel<128, 4><<<dim3(I::n_chunks * 4, ks.K), 256, 0, ts>>>(ks, img);
-    VM_CUDA(cudaGetLastError());
     const int smem_tc = tck::Smem<128, 4>::total;
     VM_CUDA(cudaFuncSetAttribute(tck::tc_train_kernel<128, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_tc));
     tck::tc_train_kernel<128, 4><<<ks.K * ks.P, tck::kTCThreads, smem_tc, ts>>>(pl.kp, i, img);
     VM_CUDA(cudaGetLastError());
-    if (g_prof.on) g_prof.kernels += 2;
+    if (g_prof.on) g_prof.kernels += 1;
   }
   if (kt1) VM_CUDA(cudaEventRecord(kt1, ts));
   if (fn) {

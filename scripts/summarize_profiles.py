@@ -17,7 +17,10 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "sm__sass_thread_inst_executed_op_ffma_pred_on.sum.peak_sustained",
         "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "smsp__sass_inst_executed_op_shared_ld.sum",
         "smsp__inst_executed.sum", "launch__registers_per_thread", "launch__shared_mem_per_block_dynamic",
-        "launch__grid_size", "launch__block_size", "lts__t_sector_hit_rate.pct"]
+        "launch__grid_size", "launch__block_size", "lts__t_sector_hit_rate.pct",
+        "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+        "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
+        "sm__inst_executed_pipe_uniform.avg.pct_of_peak_sustained_active"]
 
 
 def raw(rep):
@@ -36,11 +39,14 @@ def stalls(d):
 
 lines = [f"# ncu summary ({tag})", "",
          "Captured with `ncu --set full --clock-control none --import-source on` on one B200 under gpurun,",
-         "command `python bench.py --steps 2 --warmup 3 --no-cpu-baseline` (config 2), one launch per kernel.",
+         "command `python bench.py --steps 2 --warmup 3 --no-cpu-baseline` (config 2), one launch per kernel",
+         "(KT and KF normally run concurrently on two streams; ncu serialises them).",
          "ncu flushes caches before each replay: durations are cold-cache and serialised.", ""]
 traffic = {}
-for name, rep in (("fused MLP train (KF, mlp_kernel)", "prof_mlp"), ("sampler rays (KS)", "prof_rays"),
-                  ("Adam (KA)", "prof_adam")):
+for name, rep in (("tensor-core MLP train (KT, tc_train_kernel, hidden-128 background)", "prof_tc"),
+                  ("FFMA MLP train (KF, mlp_kernel, hidden-32 objects)", "prof_mlp"),
+                  ("partial-gradient reduce (reduce_partials_kernel)", "prof_red"),
+                  ("sampler rays (KS)", "prof_rays"), ("Adam (KA)", "prof_adam")):
     p = ROOT / "gpurun_out" / f"{rep}.ncu-rep"
     if not p.exists():
         continue
@@ -51,9 +57,11 @@ for name, rep in (("fused MLP train (KF, mlp_kernel)", "prof_mlp"), ("sampler ra
             lines.append(f"| {k} | {d[k][0]} | {d[k][1]} |")
     lines += ["", "Top warp stall reasons (share of samples): " +
               ", ".join(f"{k} {v:.1f}%" for k, v in stalls(d)), ""]
-    if rep == "prof_mlp":
-        mb = lambda k: float(d[k][0].replace(",", "")) * (1e6 if d[k][1] == "Mbyte" else 1e3 if d[k][1] == "Kbyte" else 1)
-        traffic["mlp_kernel_dram_bytes_per_launch"] = mb("dram__bytes_read.sum") + mb("dram__bytes_write.sum")
+    mb = lambda k: float(d[k][0].replace(",", "")) * (1e9 if d[k][1] == "Gbyte" else 1e6 if d[k][1] == "Mbyte"
+                                                      else 1e3 if d[k][1] == "Kbyte" else 1)
+    if rep in ("prof_mlp", "prof_tc"):
+        key = "mlp_kernel_dram_bytes_per_launch" if rep == "prof_mlp" else "tc_train_kernel_dram_bytes_per_launch"
+        traffic[key] = mb("dram__bytes_read.sum") + mb("dram__bytes_write.sum")
         traffic["source"] = f"profiles/{tag}_summary.md (ncu --set full, cold cache)"
 summ = ROOT / "gpurun_out" / "launches_summary.txt"
 if summ.exists():

@@ -505,6 +505,22 @@ __global__ void __launch_bounds__(kTCThreads, 1)
         v[16 + j] = __uint_as_float(r2[j]);
       }
     };
+    // two 32-column groups with one wait (TMEM load latency paid once)
+    auto ld64 = [&](uint32_t ta, uint32_t tb, float (&va)[32], float (&vb)[32]) {
+      uint32_t r0[16], r1[16], r2[16], r3[16];
+      VM_TMEM_LD16(ta, r0);
+      VM_TMEM_LD16(ta + 16, r1);
+      VM_TMEM_LD16(tb, r2);
+      VM_TMEM_LD16(tb + 16, r3);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        va[j] = __uint_as_float(r0[j]);
+        va[16 + j] = __uint_as_float(r1[j]);
+        vb[j] = __uint_as_float(r2[j]);
+        vb[16 + j] = __uint_as_float(r3[j]);
+      }
+    };
     auto st32 = [&](uint32_t ta, const float (&v)[32]) {
       uint32_t r[16], r2[16];
 #pragma unroll
@@ -540,9 +556,9 @@ __global__ void __launch_bounds__(kTCThreads, 1)
       // registers; the next layer's chunks (32 columns each) are staged by
       // the half that owns them, the other half only releases the slot.
       float x[2][32];
+      ld64(R(0) + c0, R(0) + c0 + 32, x[0], x[1]);
 #pragma unroll
       for (int g = 0; g < 2; ++g) {
-        ld32(R(0) + c0 + 32 * g, x[g]);
 #pragma unroll
         for (int j = 0; j < 32; ++j) x[g][j] = relu_np(x[g][j] + sBias[l * H + c0 + 32 * g + j]);
         st32(R(l + 1) + c0 + 32 * g, x[g]);
@@ -662,10 +678,11 @@ __global__ void __launch_bounds__(kTCThreads, 1)
     for (int c = 0; c < 4; ++c) {
       uint8_t* sl = acquire();
       if (q == c) {
+        float xv[2][32];
+        ld64(R(L - 1) + c0, R(L - 1) + c0 + 32, xv[0], xv[1]);
 #pragma unroll
         for (int g = 0; g < 2; ++g) {
-          float v[32];
-          ld32(R(L - 1) + c0 + 32 * g, v);
+          float (&v)[32] = xv[g];
           put_mn(sl, c0 + 32 * g, v);  // A = X3 (M = fan-in)
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
@@ -715,10 +732,11 @@ __global__ void __launch_bounds__(kTCThreads, 1)
         if (q == c) {
           uint8_t* gt = (l == 0) ? sl : sl + kHalfSlot;  // G tile
           uint8_t* xt = (l == 0) ? sl + kHalfSlot : sl;  // X tile
+          float gv2[2][32];
+          ld64(R(l + 1) + c0, R(l + 1) + c0 + 32, gv2[0], gv2[1]);
 #pragma unroll
           for (int g = 0; g < 2; ++g) {
-            float v[32];
-            ld32(R(l + 1) + c0 + 32 * g, v);
+            float (&v)[32] = gv2[g];
             if (l == 0) {
 #pragma unroll
               for (int j = 0; j < 32; ++j) put_t(gt, H, c0 + 32 * g + j, v[j]);
@@ -734,12 +752,10 @@ __global__ void __launch_bounds__(kTCThreads, 1)
             for (int i = 0; i < kN0; ++i)
               if (i / (kN0 / 2) == h) put_t(xt, kN0, i, i < kK0 ? x0[i < kK0 ? i : 0] : 0.f);
           } else {
-#pragma unroll
-            for (int g = 0; g < 2; ++g) {
-              float v[32];
-              ld32(R(l) + c0 + 32 * g, v);
-              put_mn(xt, c0 + 32 * g, v);
-            }
+            float xv[2][32];
+            ld64(R(l) + c0, R(l) + c0 + 32, xv[0], xv[1]);
+            put_mn(xt, c0, xv[0]);
+            put_mn(xt, c0 + 32, xv[1]);
           }
         }
         release();
@@ -773,8 +789,7 @@ __global__ void __launch_bounds__(kTCThreads, 1)
       // owning those columns), B = W_l^T chunks (TMA)
       {
         float gv[2][32];
-        ld32(R(l + 1) + c0, gv[0]);
-        ld32(R(l + 1) + c0 + 32, gv[1]);
+        ld64(R(l + 1) + c0, R(l + 1) + c0 + 32, gv[0], gv[1]);
 #pragma unroll 1
         for (int c = 0; c < H / 32; ++c) {
           uint8_t* sl = acquire_w(I::dx_off(l) + c * I::kC32, I::kC32);
@@ -791,8 +806,7 @@ __global__ void __launch_bounds__(kTCThreads, 1)
 #pragma unroll
       for (int g = 0; g < 2; ++g) {
         float d[32], a[32];
-        ld32(R(0) + c0 + 32 * g, d);
-        ld32(R(l) + c0 + 32 * g, a);
+        ld64(R(0) + c0 + 32 * g, R(l) + c0 + 32 * g, d, a);
 #pragma unroll
         for (int j = 0; j < 32; ++j) d[j] = a[j] > 0.f ? d[j] : 0.f;
         st32(R(l) + c0 + 32 * g, d);

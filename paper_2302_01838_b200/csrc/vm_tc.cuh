@@ -1,18 +1,16 @@
-// tcgen05 / TMEM / mbarrier primitives for sm_100a (inline PTX), and the
-// shared-memory operand layout used by the tensor-core MLP kernel (KT).
+// tcgen05 / TMEM / mbarrier / TMA-bulk primitives for sm_100a (inline PTX)
+// used by the tensor-core MLP kernel KT (vm_tc_mlp.cuh).
 //
-// Operand layout ("core-matrix interleaved", SWIZZLE_NONE): a logical
-// [rows][cols] fp32 tile is stored as 8x4 core matrices of 128 contiguous
-// bytes (8 rows x 16 B).  Element (r, c) lives at
-//     (r / 8) * rstride + (c / 4) * 128 + (r % 8) * 16 + (c % 4) * 4
-// with rstride = 128 * cols / 4 (column groups of one row group adjacent).
-// The same bytes serve as a K-major operand (rows = M/N, cols = K) and as an
-// MN-major operand (rows = K, cols = M/N): for K-major the descriptor's
-// SBO is the 8-row-group stride and LBO the 4-column-group stride (128 B);
-// for MN-major SBO is the 4-column-group stride (128 B) and LBO the 8-row
-// (K) group stride.  That is what lets one staged activation or weight tile
-// feed the forward GEMM, the input-gradient GEMM and the weight-gradient
-// GEMM without a transposed copy.
+// Shared-memory operand layouts verified on a B200 by scripts/tc_probe.cu
+// (kind::tf32, fp32 accumulate):
+//  * "interleaved" SWIZZLE_NONE K-major: a [rows][cols] tile stored as 8x4
+//    core matrices of 128 contiguous bytes, element (r, c) at
+//        (r / 8) * (cols * 32) + (c / 4) * 128 + (r % 8) * 16 + (c % 4) * 4,
+//    descriptor LBO = 128 (next 4-column group), SBO = cols * 32 (next 8 rows);
+//  * SWIZZLE_128B K-major (32-column rows of 128 B, 16-B chunks XOR row % 8);
+//  * MN-major tf32 only in SWIZZLE_128B_BASE32B (see vm_tc_mlp.cuh mn_off);
+//    SWIZZLE_NONE MN-major tf32 operands read as zeros.
+// M = 128 MMAs need N % 16 == 0.
 #pragma once
 
 #include <cstdint>

@@ -129,3 +129,23 @@ def test_tensor_core_gradient_accuracy(cuda):
         assert np.linalg.norm(g - t) / np.linalg.norm(t) < 2e-5, f"layer {l}"
         gb = sb.m_biases[l][:k].cpu().numpy().astype(np.float64)[0]
         assert np.linalg.norm(gb - ob.mb[l][0]) / np.linalg.norm(ob.mb[l][0]) < 2e-5, f"bias {l}"
+
+
+@pytest.mark.parametrize("k,rays,points", [(2, 50, 7), (3, 13, 10), (1, 12, 10), (2, 37, 16)])
+def test_tensor_core_partial_tiles_and_sample_counts(cuda, k, rays, points):
+    """KT edge cases: several hidden-128 models in one stack, a partial last
+    tile (rays % floor(128/S) != 0), a single-tile model (finalised in the
+    kernel itself) and S != 10 (generic render chain)."""
+    arch = ModelArch(n_layers=4, hidden=128, n_freq=5)
+    params, state = init_stacked(arch, k, seed=5)
+    ost = O.new_stack(oracle_arch(arch), k, 5)
+    batch = _synthetic_batch(arch, k, rays, points, seed=9)
+    hb = to_host_batch(batch)
+    for step in range(5):
+        ld, lc, lo = train_on_batch(params, state, batch, LossWeights())
+        ed, ec, eo = O.train_on_batch(ost, hb)
+        np.testing.assert_allclose(ld, ed, rtol=1e-4, atol=1e-6)
+        np.testing.assert_allclose(lc, ec, rtol=1e-4, atol=1e-6)
+        np.testing.assert_allclose(lo, eo, rtol=1e-4, atol=1e-6)
+    assert_params_rel_l2(params, ost)
+    np.testing.assert_array_equal(state.step[:k].cpu().numpy(), ost.step[:k])

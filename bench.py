@@ -254,7 +254,7 @@ def main():
     mlp_ms = C.c_double()
     lib.vm_profile_read(C.byref(n_launch), C.byref(mlp_ms))
     per_tag = {}
-    for tag in (1, 2):  # 1: FFMA kernel KF (objects), 2: tensor-core branch KT (background)
+    for tag in (1, 2, 3):  # 1: FFMA kernel KF (objects), 2: tensor-core branch KT (background), 3: reduce + Adam
         n_t, ms_t = C.c_int(), C.c_double()
         lib.vm_profile_read_tag(tag, C.byref(n_t), C.byref(ms_t))
         per_tag[tag] = ms_t.value / n_t.value if n_t.value else None
@@ -351,7 +351,8 @@ def main():
             "roofline": dominant,
             "roofline_kernels": kernels,
             "mlp_phase": {"ms": kernel_ms, "flop": flop_launch,
-                          "achieved_tflops": flop_launch / (kernel_ms * 1e-3) / 1e12},
+                          "achieved_tflops": flop_launch / (kernel_ms * 1e-3) / 1e12,
+                          "reduce_adam_ms": per_tag.get(3)},
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
         }

@@ -109,6 +109,46 @@ __device__ float pairwise_sum(const F& get, int64_t n) {
   return pairwise_sum_rec(get, 0, n);
 }
 
+// The leaves (n <= 128 blocks) of pairwise_sum_rec's recursion for n
+// elements, in depth-first order; returns their count (only the first
+// max_leaves are stored).  Lets a CTA sum the leaves in parallel and combine
+// them with pairwise_combine in exactly the recursive order.
+__device__ inline int pairwise_leaves(int64_t n, int64_t* start, int* len, int max_leaves) {
+  int64_t si[24], sn[24];  // depth <= log2(n / 128) + 1 <= 24 for any int32 row count
+  int sp = 0, cnt = 0;
+  si[sp] = 0;
+  sn[sp++] = n;
+  while (sp > 0) {
+    --sp;
+    const int64_t i0 = si[sp], m = sn[sp];
+    if (m <= 128) {
+      if (cnt < max_leaves) {
+        start[cnt] = i0;
+        len[cnt] = int(m);
+      }
+      ++cnt;
+    } else {
+      int64_t m2 = m / 2;
+      m2 -= m2 % 8;
+      si[sp] = i0 + m2;  // right half, popped after the left one
+      sn[sp++] = m - m2;
+      si[sp] = i0;
+      sn[sp++] = m2;
+    }
+  }
+  return cnt;
+}
+
+// Adds per-leaf sums (depth-first order) the way pairwise_sum_rec adds halves.
+__device__ inline float pairwise_combine(int64_t n, const float* leaf, int& next) {
+  if (n <= 128) return leaf[next++];
+  int64_t n2 = n / 2;
+  n2 -= n2 % 8;
+  const float a = pairwise_combine(n2, leaf, next);
+  const float b = pairwise_combine(n - n2, leaf, next);
+  return __fadd_rn(a, b);
+}
+
 // np.sign for float32: +1, -1, 0 for +-0, NaN for NaN.
 __device__ __forceinline__ float np_sign(float x) {
   return x > 0.f ? 1.f : (x < 0.f ? -1.f : (x == 0.f ? 0.f : x));

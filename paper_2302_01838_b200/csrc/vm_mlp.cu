@@ -86,6 +86,9 @@ __device__ __forceinline__ void load_block(const KStack& st, int k, int64_t gs0,
 __device__ void finalize_model(const KStack& st, int k, bool all_finite, bool meta, float* scratch,
                                int scratch_floats) {
   const int tid = threadIdx.x;
+  // non-meta CTAs only need the update mask when their chunk is non-finite
+  // (both conditions are CTA-uniform, so the barrier below is too)
+  if (!meta && all_finite) return;
   bool any_ok = false;
   for (int r = tid; r < st.R; r += blockDim.x) any_ok |= st.ok[int64_t(k) * st.R + r] != 0;
   const bool upd = __syncthreads_or(any_ok);
@@ -100,7 +103,31 @@ __device__ void finalize_model(const KStack& st, int k, bool all_finite, bool me
     for (int i = tid; i < st.R * 3; i += blockDim.x) scratch[i] = __ldcg(terms + i);
     __syncthreads();
   }
-  if (tid < 3) {
+  // more than one pairwise leaf: the leaves (<= 128 rays each) are summed by
+  // separate threads, then combined in the recursion's order (same bits)
+  constexpr int kMaxLeaves = 64;
+  __shared__ int64_t lf_start[kMaxLeaves];
+  __shared__ int lf_len[kMaxLeaves];
+  __shared__ float lf_sum[3][kMaxLeaves];
+  __shared__ int lf_n;
+  const bool parallel = staged && st.R > 128 && 3 * kMaxLeaves <= int(blockDim.x);
+  if (parallel) {
+    if (tid == 0) lf_n = pairwise_leaves(st.R, lf_start, lf_len, kMaxLeaves);
+    __syncthreads();
+  }
+  if (parallel && lf_n <= kMaxLeaves) {
+    if (tid < 3 * lf_n) {
+      const int j = tid % 3, lf = tid / 3;
+      lf_sum[j][lf] = pairwise_sum_leaf([&](int64_t r) { return scratch[r * 3 + j]; }, lf_start[lf], lf_len[lf]);
+    }
+    __syncthreads();
+    if (tid < 3) {
+      int next = 0;
+      const float sum = pairwise_combine(st.R, lf_sum[tid], next);
+      st.losses[int64_t(k) * 3 + tid] = sum;
+      if (!isfinite(sum)) atomicMin(&st.status[1], k);
+    }
+  } else if (tid < 3) {
     const int j = tid;
     const float sum = staged ? pairwise_sum([&](int64_t r) { return scratch[r * 3 + j]; }, st.R)
                              : pairwise_sum([&](int64_t r) { return __ldcg(terms + r * 3 + j); }, st.R);
@@ -134,25 +161,52 @@ constexpr int kRedChunk = kRedThreads / kRedGroups * 4;       // floats per redu
 
 // Sum the P partial gradient blocks of every split model in a fixed order
 // (deterministic): group q of the CTA adds partials [q*P/8, (q+1)*P/8)
-// sequentially (all loads of a batch issued before the adds, so a thread has
-// up to 16 L2 requests in flight), then the eight group sums are added in
+// sequentially (loads issued in batches of 6 before the adds; few registers
+// so 6 CTAs fit an SM), then the eight group sums are added in
 // group order through shared memory.  One CTA per (model, 128-float chunk);
 // chunk 0 also finalises the model.
-__global__ void __launch_bounds__(kRedThreads) reduce_partials_kernel(const __grid_constant__ KParams p) {
+__host__ __device__ inline int red_chunk_floats(int P) { return P <= kRedGroups ? kRedThreads * 4 : kRedChunk; }
+
+__global__ void __launch_bounds__(kRedThreads, 6) reduce_partials_kernel(const __grid_constant__ KParams p) {
   extern __shared__ __align__(16) float red_smem[];
   __shared__ float4 gsum[kRedGroups][kRedChunk / 4];
   int b = blockIdx.x, si = 0;
   for (; si < p.n_stacks; ++si) {
     const KStack& s = p.s[si];
     if (s.P <= 1) continue;
-    const int n = s.K * ((s.block + kRedChunk - 1) / kRedChunk);
+    const int cf = red_chunk_floats(s.P);
+    const int n = s.K * ((s.block + cf - 1) / cf);
     if (b < n) break;
     b -= n;
   }
   if (si >= p.n_stacks) return;
   const KStack& st = p.s[si];
-  const int chunks = (st.block + kRedChunk - 1) / kRedChunk;
+  const int cf = red_chunk_floats(st.P);
+  const int chunks = (st.block + cf - 1) / cf;
   const int k = b / chunks, ch = b % chunks;
+  bool finite = true;
+  if (st.P <= kRedGroups) {
+    // few partials (split FFMA items): one thread per float4, partials in order
+    const int i = ch * cf + 4 * threadIdx.x;
+    if (i < st.block) {
+      const float* pb = st.partials + int64_t(k) * st.P * st.block + i;
+      float4 w[kRedGroups];
+#pragma unroll
+      for (int u = 0; u < kRedGroups; ++u)
+        if (u < st.P) w[u] = __ldcg(reinterpret_cast<const float4*>(pb + int64_t(u) * st.block));
+      float4 tot = w[0];
+#pragma unroll
+      for (int u = 1; u < kRedGroups; ++u)
+        if (u < st.P) {
+          tot.x += w[u].x; tot.y += w[u].y; tot.z += w[u].z; tot.w += w[u].w;
+        }
+      st4(st.grads + int64_t(k) * st.block + i, tot);
+      finite = isfinite(tot.x) && isfinite(tot.y) && isfinite(tot.z) && isfinite(tot.w);
+    }
+    const bool all_finite = __syncthreads_and(finite);
+    finalize_model(st, k, all_finite, ch == 0, red_smem, st.R * 3);
+    return;
+  }
   const int col = threadIdx.x % (kRedChunk / 4), q = threadIdx.x / (kRedChunk / 4);
   const int i = ch * kRedChunk + 4 * col;
   const int per = (st.P + kRedGroups - 1) / kRedGroups;
@@ -163,28 +217,22 @@ __global__ void __launch_bounds__(kRedThreads) reduce_partials_kernel(const __gr
     const int64_t stride = st.block;
     v = __ldcg(reinterpret_cast<const float4*>(pb + p0 * stride));
     int pp = p0 + 1;
-    for (; pp + 16 <= p1; pp += 16) {
-      float4 w[16];
+    for (; pp + 6 <= p1; pp += 6) {
+      float4 w[6];
 #pragma unroll
-      for (int u = 0; u < 16; ++u) w[u] = __ldcg(reinterpret_cast<const float4*>(pb + (pp + u) * stride));
+      for (int u = 0; u < 6; ++u) w[u] = __ldcg(reinterpret_cast<const float4*>(pb + (pp + u) * stride));
 #pragma unroll
-      for (int u = 0; u < 16; ++u) {
+      for (int u = 0; u < 6; ++u) {
         v.x += w[u].x; v.y += w[u].y; v.z += w[u].z; v.w += w[u].w;
       }
     }
-    float4 w[16];
-#pragma unroll
-    for (int u = 0; u < 16; ++u)
-      if (pp + u < p1) w[u] = __ldcg(reinterpret_cast<const float4*>(pb + (pp + u) * stride));
-#pragma unroll
-    for (int u = 0; u < 16; ++u)
-      if (pp + u < p1) {
-        v.x += w[u].x; v.y += w[u].y; v.z += w[u].z; v.w += w[u].w;
-      }
+    for (; pp < p1; ++pp) {
+      const float4 w = __ldcg(reinterpret_cast<const float4*>(pb + pp * stride));
+      v.x += w.x; v.y += w.y; v.z += w.z; v.w += w.w;
+    }
   }
   gsum[q][col] = v;
   __syncthreads();
-  bool finite = true;
   if (q == 0 && i < st.block) {
     float4 tot = gsum[0][col];
 #pragma unroll
@@ -656,7 +704,8 @@ struct KernelProfiler {
   bool on = false;
   long kernels = 0;  // every kernel launched by vm_train_step / vm_sample while on
   std::vector<cudaEvent_t> ev;  // start/stop pairs
-  std::vector<int> tag;         // per pair: 0 = MLP phase, 1 = FFMA kernel (KF), 2 = tensor-core branch (KT)
+  std::vector<int> tag;         // per pair: 0 = MLP phase, 1 = FFMA kernel (KF), 2 = tensor-core branch (KT),
+                                // 3 = partial reduce + Adam
   size_t used = 0;
   cudaEvent_t get() {
     if (used == ev.size()) {
@@ -904,9 +953,17 @@ extern "C" int vm_train_step(const VmStack* stacks, const VmBatch* batches, int 
     VM_CUDA(cudaStreamWaitEvent(s, ev_join, 0));
   }
   if (g_prof.on) VM_CUDA(cudaEventRecord(e1, s));
+  cudaEvent_t r0 = nullptr, r1 = nullptr;
+  if (g_prof.on) {
+    g_prof.pair(r0, r1, 3);
+    VM_CUDA(cudaEventRecord(r0, s));
+  }
   int red_grid = 0;
   for (int i = 0; i < n_stacks; ++i)
-    if (pl.kp.s[i].P > 1) red_grid += pl.kp.s[i].K * ((pl.kp.s[i].block + kRedChunk - 1) / kRedChunk);
+    if (pl.kp.s[i].P > 1) {
+      const int cf = red_chunk_floats(pl.kp.s[i].P);
+      red_grid += pl.kp.s[i].K * ((pl.kp.s[i].block + cf - 1) / cf);
+    }
   if (red_grid > 0) {
     int red_smem = 0;
     for (int i = 0; i < n_stacks; ++i)
@@ -922,6 +979,7 @@ extern "C" int vm_train_step(const VmStack* stacks, const VmBatch* batches, int 
     VM_CUDA(cudaGetLastError());
     if (g_prof.on) g_prof.kernels += 1;
   }
+  if (r1) VM_CUDA(cudaEventRecord(r1, s));
   return VM_OK;
 }
 

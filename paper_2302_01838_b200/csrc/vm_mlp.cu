@@ -156,16 +156,17 @@ __device__ void finalize_model(const KStack& st, int k, bool all_finite, bool me
 namespace vm {
 
 constexpr int kRedThreads = 256;
-constexpr int kRedGroups = 8;                                 // partial groups per output column
-constexpr int kRedChunk = kRedThreads / kRedGroups * 4;       // floats per reduce CTA (128)
+constexpr int kRedDirect = 8;                                 // P <= 8: one thread sums a float4's partials
+constexpr int kRedGroups = 16;                                // partial groups per output column (P > 8)
+constexpr int kRedChunk = kRedThreads / kRedGroups * 4;       // floats per reduce CTA (64)
 
 // Sum the P partial gradient blocks of every split model in a fixed order
-// (deterministic): group q of the CTA adds partials [q*P/8, (q+1)*P/8)
+// (deterministic): group q of the CTA adds partials [q*P/16, (q+1)*P/16)
 // sequentially (loads issued in batches of 6 before the adds; few registers
-// so 6 CTAs fit an SM), then the eight group sums are added in
-// group order through shared memory.  One CTA per (model, 128-float chunk);
+// so 6 CTAs fit an SM), then the 16 group sums are added in
+// group order through shared memory.  One CTA per (model, 64-float chunk);
 // chunk 0 also finalises the model.
-__host__ __device__ inline int red_chunk_floats(int P) { return P <= kRedGroups ? kRedThreads * 4 : kRedChunk; }
+__host__ __device__ inline int red_chunk_floats(int P) { return P <= kRedDirect ? kRedThreads * 4 : kRedChunk; }
 
 __global__ void __launch_bounds__(kRedThreads, 6) reduce_partials_kernel(const __grid_constant__ KParams p) {
   extern __shared__ __align__(16) float red_smem[];
@@ -185,18 +186,18 @@ __global__ void __launch_bounds__(kRedThreads, 6) reduce_partials_kernel(const _
   const int chunks = (st.block + cf - 1) / cf;
   const int k = b / chunks, ch = b % chunks;
   bool finite = true;
-  if (st.P <= kRedGroups) {
+  if (st.P <= kRedDirect) {
     // few partials (split FFMA items): one thread per float4, partials in order
     const int i = ch * cf + 4 * threadIdx.x;
     if (i < st.block) {
       const float* pb = st.partials + int64_t(k) * st.P * st.block + i;
-      float4 w[kRedGroups];
+      float4 w[kRedDirect];
 #pragma unroll
-      for (int u = 0; u < kRedGroups; ++u)
+      for (int u = 0; u < kRedDirect; ++u)
         if (u < st.P) w[u] = __ldcg(reinterpret_cast<const float4*>(pb + int64_t(u) * st.block));
       float4 tot = w[0];
 #pragma unroll
-      for (int u = 1; u < kRedGroups; ++u)
+      for (int u = 1; u < kRedDirect; ++u)
         if (u < st.P) {
           tot.x += w[u].x; tot.y += w[u].y; tot.z += w[u].z; tot.w += w[u].w;
         }

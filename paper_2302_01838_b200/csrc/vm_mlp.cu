@@ -168,13 +168,14 @@ constexpr int kRedChunk = kRedThreads / kRedGroups * 4;       // floats per redu
 // chunk 0 also finalises the model.
 __host__ __device__ inline int red_chunk_floats(int P) { return P <= kRedDirect ? kRedThreads * 4 : kRedChunk; }
 
-__global__ void __launch_bounds__(kRedThreads, 6) reduce_partials_kernel(const __grid_constant__ KParams p) {
+__global__ void __launch_bounds__(kRedThreads, 6) reduce_partials_kernel(const __grid_constant__ KParams p,
+                                                                          int only_stack) {
   extern __shared__ __align__(16) float red_smem[];
   __shared__ float4 gsum[kRedGroups][kRedChunk / 4];
   int b = blockIdx.x, si = 0;
   for (; si < p.n_stacks; ++si) {
     const KStack& s = p.s[si];
-    if (s.P <= 1) continue;
+    if (s.P <= 1 || (only_stack >= 0 && si != only_stack)) continue;
     const int cf = red_chunk_floats(s.P);
     const int n = s.K * ((s.block + cf - 1) / cf);
     if (b < n) break;
@@ -555,8 +556,8 @@ struct AdamParams {
   int n_stacks;
 };
 
-__global__ void __launch_bounds__(256) adam_train_kernel(const __grid_constant__ AdamParams p) {
-  int b = blockIdx.x, si = 0;
+__global__ void __launch_bounds__(256) adam_train_kernel(const __grid_constant__ AdamParams p, int block_offset) {
+  int b = blockIdx.x + block_offset, si = 0;
   if (p.n_stacks > 1 && b >= p.s[1].item_base) si = 1;
   const AdamStack& s = p.s[si];
   b -= s.item_base;
@@ -818,6 +819,31 @@ int plan_train(const VmStack* stacks, const VmBatch* batches, int n, TrainPlan& 
   pl.ws_bytes = off;
   return VM_OK;
 }
+// Partial reduce + Adam for stacks [first, last) on stream s.  Adam of stack
+// i reads the status words of stacks < i (trainer.py:368-388 raise order), so
+// a prefix of stacks can be finished before later stacks are done.
+int reduce_and_adam(const TrainPlan& pl, int n_stacks, int first, int last, cudaStream_t s) {
+  for (int i = first; i < last; ++i) {
+    const KStack& ks = pl.kp.s[i];
+    if (ks.P <= 1 || ks.K == 0) continue;
+    const int cf = red_chunk_floats(ks.P);
+    const int grid = ks.K * ((ks.block + cf - 1) / cf);
+    const int red_smem = ks.R * 3 * 4;
+    if (red_smem > 48 * 1024)
+      VM_CUDA(cudaFuncSetAttribute(reduce_partials_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, red_smem));
+    reduce_partials_kernel<<<grid, kRedThreads, red_smem, s>>>(pl.kp, i);
+    VM_CUDA(cudaGetLastError());
+    if (g_prof.on) g_prof.kernels += 1;
+  }
+  const int b0 = pl.ap.s[first].item_base;
+  const int b1 = (last < n_stacks) ? pl.ap.s[last].item_base : pl.adam_grid;
+  if (b1 > b0) {
+    adam_train_kernel<<<b1 - b0, 256, 0, s>>>(pl.ap, b0);
+    VM_CUDA(cudaGetLastError());
+    if (g_prof.on) g_prof.kernels += 1;
+  }
+  return VM_OK;
+}
 }  // namespace
 
 extern "C" size_t vm_train_workspace_bytes(const VmStack* stacks, const VmBatch* batches, int n_stacks) {
@@ -949,7 +975,15 @@ extern "C" int vm_train_step(const VmStack* stacks, const VmBatch* batches, int 
       VM_CUDA(cudaEventRecord(kf1, s));
     }
   }
+  // stacks before the first tensor-core stack are finished on the main
+  // stream while the KT branch is still running
+  int tail_from = 0;
   if (forked) {
+    while (tail_from < n_stacks && !pl.kp.s[tail_from].tc) ++tail_from;
+    if (tail_from > 0) {
+      rc = reduce_and_adam(pl, n_stacks, 0, tail_from, s);
+      if (rc) return rc;
+    }
     VM_CUDA(cudaEventRecord(ev_join, side));
     VM_CUDA(cudaStreamWaitEvent(s, ev_join, 0));
   }
@@ -959,26 +993,9 @@ extern "C" int vm_train_step(const VmStack* stacks, const VmBatch* batches, int 
     g_prof.pair(r0, r1, 3);
     VM_CUDA(cudaEventRecord(r0, s));
   }
-  int red_grid = 0;
-  for (int i = 0; i < n_stacks; ++i)
-    if (pl.kp.s[i].P > 1) {
-      const int cf = red_chunk_floats(pl.kp.s[i].P);
-      red_grid += pl.kp.s[i].K * ((pl.kp.s[i].block + cf - 1) / cf);
-    }
-  if (red_grid > 0) {
-    int red_smem = 0;
-    for (int i = 0; i < n_stacks; ++i)
-      if (pl.kp.s[i].P > 1) red_smem = std::max(red_smem, pl.kp.s[i].R * 3 * 4);
-    if (red_smem > 48 * 1024)
-      VM_CUDA(cudaFuncSetAttribute(reduce_partials_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, red_smem));
-    reduce_partials_kernel<<<red_grid, kRedThreads, red_smem, s>>>(pl.kp);
-    VM_CUDA(cudaGetLastError());
-    if (g_prof.on) g_prof.kernels += 1;
-  }
   if (pl.adam_grid > 0) {
-    adam_train_kernel<<<pl.adam_grid, 256, 0, s>>>(pl.ap);
-    VM_CUDA(cudaGetLastError());
-    if (g_prof.on) g_prof.kernels += 1;
+    rc = reduce_and_adam(pl, n_stacks, tail_from, n_stacks, s);
+    if (rc) return rc;
   }
   if (r1) VM_CUDA(cudaEventRecord(r1, s));
   return VM_OK;

@@ -299,10 +299,12 @@ def main():
     flop_bg = (cfg.rays_background * cfg.points_per_ray * flop_per_sample(128)) if cfg.train_background else 0
     flop_launch = flop_obj + flop_bg
     kernel_ms = mlp_ms.value / max(n_launch.value, 1)
-    traffic = None
+    traffic = traffic_tc = None
     tf_path = ROOT / "profiles" / "traffic.json"
     if tf_path.exists():
-        traffic = json.loads(tf_path.read_text()).get("mlp_kernel_dram_bytes_per_launch")
+        tj = json.loads(tf_path.read_text())
+        traffic = tj.get("mlp_kernel_dram_bytes_per_launch")
+        traffic_tc = tj.get("tc_train_kernel_dram_bytes_per_launch")
     peaks_path = ROOT / "MEASURED_PEAKS.json"
     bf16 = json.loads(peaks_path.read_text()).get("bf16_tflops") if peaks_path.exists() else None
     tf32_peak = (bf16 if bf16 else 1590.0) / 2.0
@@ -319,7 +321,7 @@ def main():
     if per_tag.get(2) and flop_bg:
         a = flop_bg / (per_tag[2] * 1e-3) / 1e12
         kernels.append({"bound": "tensor", "achieved": a, "peak": tf32_peak, "unit": "TFLOP/s", "frac": a / tf32_peak,
-                        "traffic": None, "kernel": "tc_train_kernel (KT, tcgen05 3xTF32, hidden-128 background)",
+                        "traffic": traffic_tc, "kernel": "tc_train_kernel (KT, tcgen05 3xTF32, hidden-128 background)",
                         "kernel_ms": per_tag[2], "flop_per_launch": flop_bg,
                         "note": "3xTF32 issues 3 MMAs per algorithmic product; tensor-pipe FLOPs = 3x achieved",
                         "peak_source": tf32_src})

@@ -107,24 +107,28 @@ def build_tables(arena: KeyframeArena, instances, bound_pad: float, frozen=None,
     n = len(instances)
     objs = np.zeros(max(n, 1), OBJ_DTYPE)
     parts = []
-    begin = 0
-    mins = np.empty((n, 3))
-    maxs = np.empty((n, 3))
+    n_kf, mins, maxs, ids, active, scale = [], [], [], [], [], []
     for k, inst in enumerate(instances):
         kfs = inst.keyframes
         for kf in kfs:
             if getattr(kf, "texel_off", -1) < 0:
                 arena.add(kf)
             parts.append(_kf_desc(kf))
-        objs["kf_begin"][k] = begin
-        objs["n_kf"][k] = len(kfs)
-        begin += len(kfs)
-        mins[k] = inst.aabb.min
-        maxs[k] = inst.aabb.max
-        objs["object_id"][k] = inst.object_id
-        objs["active"][k] = 1 if (inst.active and not (frozen is not None and frozen[k])) else 0
-        objs["pe_scale"][k] = inst.pe_scale
-    if n:
+        n_kf.append(len(kfs))
+        mins.append(inst.aabb.min)
+        maxs.append(inst.aabb.max)
+        ids.append(inst.object_id)
+        active.append(1 if (inst.active and not (frozen is not None and frozen[k])) else 0)
+        scale.append(inst.pe_scale)
+    if n:  # one vectorised fill per field (per-instance numpy scalar stores were the cost)
+        nk = np.asarray(n_kf, np.int32)
+        objs["n_kf"][:n] = nk
+        objs["kf_begin"][:n] = np.concatenate(([0], np.cumsum(nk)[:-1])).astype(np.int32)
+        objs["object_id"][:n] = ids
+        objs["active"][:n] = active
+        objs["pe_scale"][:n] = scale
+        mins = np.asarray(mins, np.float64).reshape(n, 3)
+        maxs = np.asarray(maxs, np.float64).reshape(n, 3)
         pad = bound_pad * (0.5 * (maxs - mins))
         pmin, pmax = mins - pad, maxs + pad
         objs["box_min"][:n], objs["box_max"][:n] = pmin, pmax

@@ -60,6 +60,7 @@ class Mapper:
         self._g = None          # graph-replay state (see _graph_step)
         self._dev_tables = [(DeviceTable(self.device), DeviceTable(self.device)) for _ in range(2)]
         self._dirty = True
+        self._pin_scale = None
         self._n_kf = 0
 
     # ------------------------------------------------------------ building
@@ -130,10 +131,17 @@ class Mapper:
             self._buf_obj = SampleBuffers(K, c.rays_per_object, S, c.arch_object.input_dim, False, self.device)
         if bg is not None and self._buf_bg is None:
             self._buf_bg = SampleBuffers(1, c.rays_background, S, c.arch_background.input_dim, False, self.device)
+        # PE scales through one pinned staging buffer (non-blocking uploads)
+        sc = np.array([float(i.pe_scale) for i in objs] + ([float(bg.pe_scale)] if bg is not None else []),
+                      np.float32)
+        if self._pin_scale is None or self._pin_scale.numel() < max(len(sc), 1):
+            self._pin_scale = torch.empty(max(len(sc), 64), dtype=torch.float32, pin_memory=True)
+        if len(sc):
+            self._pin_scale[:len(sc)].numpy()[:] = sc
         if K:
-            self._buf_obj.pe_scale[:K] = torch.tensor([float(i.pe_scale) for i in objs], device=self.device)
+            self._buf_obj.pe_scale[:K].copy_(self._pin_scale[:K], non_blocking=True)
         if bg is not None:
-            self._buf_bg.pe_scale[:1] = float(bg.pe_scale)
+            self._buf_bg.pe_scale[:1].copy_(self._pin_scale[K:K + 1], non_blocking=True)
         if self._g is not None:  # keep the graphs' second batch buffers' PE scales in step
             for a, b in zip(self._g["bufs"], (self._buf_obj, self._buf_bg)):
                 if a is not None and b is not None:

@@ -405,12 +405,13 @@ __global__ void __launch_bounds__(kTCThreads, 1)
       return smem + s * kSlot;
     };
     // weight chunk: after acquiring the slot (its previous use is complete, so
-    // no mbarrier phase can be skipped) one thread starts the TMA bulk copy of
-    // the pre-split weight chunk into the slot's B half; the MMA thread waits
-    // for its bytes on wfull.
-    auto acquire_w = [&](int w_off, int floats) -> uint8_t* {
+    // no mbarrier phase can be skipped) the first thread of the half that
+    // stages the chunk's A operand starts the TMA bulk copy of the pre-split
+    // weight chunk into the slot's B half, so each half's copies are issued
+    // at its own pace; the MMA thread waits for the bytes on wfull.
+    auto acquire_w = [&](int w_off, int floats, int issuer_half) -> uint8_t* {
       uint8_t* slot = acquire();
-      if (tid == 0) {
+      if (tid == issuer_half * 128) {
         uint64_t* wb = &wfull[it % kNS];
         tc::mbar_arrive_tx(wb, uint32_t(floats * 4));
         tc::bulk_g2s(slot + kHalfSlot, img + w_off, uint32_t(floats * 4), wb);
@@ -542,10 +543,10 @@ __global__ void __launch_bounds__(kTCThreads, 1)
 #pragma unroll
       for (int i = 0; i < 8; ++i) xb[i] = x0[32 + i];
       // chunk 0 (fan-in columns 0-31) by half 0, chunk 1 (32-39) by half 1
-      uint8_t* s0 = acquire_w(I::fwd_off(0), I::kC32);
+      uint8_t* s0 = acquire_w(I::fwd_off(0), I::kC32, 0);
       if (h == 0) stage_row(s0, 32, 0, xa, 8);
       release();
-      uint8_t* s1 = acquire_w(I::fwd_off(0) + I::kC32, I::kC8);
+      uint8_t* s1 = acquire_w(I::fwd_off(0) + I::kC32, I::kC8, 1);
       if (h == 1) stage_row(s1, 8, 0, xb, 2);
       release();
     }
@@ -583,7 +584,7 @@ __global__ void __launch_bounds__(kTCThreads, 1)
       }
 #pragma unroll 1
       for (int c = 0; c < H / 32; ++c) {
-        uint8_t* sl = acquire_w(I::fwd_off(l + 1) + c * I::kC32, I::kC32);
+        uint8_t* sl = acquire_w(I::fwd_off(l + 1) + c * I::kC32, I::kC32, c >> 1);
         if ((c >> 1) == h) {
           float v[32];
 #pragma unroll
@@ -792,7 +793,7 @@ __global__ void __launch_bounds__(kTCThreads, 1)
         ld64(R(l + 1) + c0, R(l + 1) + c0 + 32, gv[0], gv[1]);
 #pragma unroll 1
         for (int c = 0; c < H / 32; ++c) {
-          uint8_t* sl = acquire_w(I::dx_off(l) + c * I::kC32, I::kC32);
+          uint8_t* sl = acquire_w(I::dx_off(l) + c * I::kC32, I::kC32, c >> 1);
           if ((c >> 1) == h) {
             float v[32];
 #pragma unroll

@@ -119,11 +119,13 @@ __global__ void __launch_bounds__(256) tc_prep_kernel(const __grid_constant__ KS
 // byte offset of (row, col) in a 128B-swizzled K-major tile with 32 columns
 // 3xTF32 operand split used for staging: hi = x rounded to the nearest tf32
 // (ties away, like cvt.rna, without its inf/nan guard: a non-finite value
-// stays non-finite and is caught by the gradient check), lo = x - hi (exact)
-// rounded the same way.
+// stays non-finite and is caught by the gradient check), lo = x - hi (exact,
+// |lo| <= 2^-11 |x|); the tensor core keeps lo's top 19 bits, so the split
+// error is <= 2^-22 |x|.  Two integer ALU ops + one FADD per element: the
+// ALU pipe (2 cycles per warp instruction per SMSP) bounds the staging.
 __device__ __forceinline__ void split_fast(float x, float& hi, float& lo) {
   hi = __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
-  lo = __uint_as_float((__float_as_uint(__fsub_rn(x, hi)) + 0x1000u) & 0xFFFFE000u);
+  lo = __fsub_rn(x, hi);
 }
 
 __device__ __forceinline__ uint32_t sw128_off(int row, int col) {

@@ -4,12 +4,12 @@
 // (models.py:311-398 forward/backward, render.py:230-333 render/losses) for
 // one 128-row tile of samples (floor(128/S) whole rays) per CTA.
 //
-// Precision: every GEMM runs as 3xTF32 -- x = hi + lo with hi = rna_tf32(x),
-// lo = rna_tf32(x - hi); A.B ~= lo_A.hi_B + hi_A.lo_B + hi_A.hi_B accumulated
-// in fp32 in TMEM -- which keeps ~fp32 accuracy (probe: 3e-7 relative to
-// sum|ab| for K=32), inside the north star's 1e-4 contract.  The 4-wide
-// output layer, render, losses and their gradients run on CUDA cores in fp32
-// with the reference's operation order.
+// Precision: every GEMM runs as 3xTF32 -- x = hi + lo with hi = tf32(x)
+// (round to nearest) and lo = x - hi; A.B ~= lo_A.hi_B + hi_A.lo_B + hi_A.hi_B
+// accumulated in fp32 in TMEM (probe: 3e-7 relative to sum|ab| for K=32;
+// one-step gradients ~2e-6 relative to an f64 run), inside the north star's
+// 1e-4 contract.  The 4-wide output layer, render, losses and their gradients
+// run on CUDA cores in fp32 with the reference's operation order.
 //
 // On-chip data flow (no activation ever touches HBM):
 //  * TMEM (512 columns x 128 lanes, lane = sample row): R0 = MMA accumulator
@@ -20,14 +20,17 @@
 //    hi/lo pair).  Forward / input-gradient GEMMs stage A = activations or
 //    gradients [128 samples][32 features] (core-matrix interleaved, K-major,
 //    conflict-free float4 stores by the owning thread) and B = a pre-split,
-//    pre-laid-out weight chunk copied with cp.async from an L2-resident image
-//    (tc_prep_kernel builds it once per step).  Weight-gradient GEMMs
-//    dW = G^T X (K = samples) stage both operands transposed, 32 samples (one
-//    warp's TMEM lanes) per chunk, as 128B-swizzled K-major tiles written
-//    with conflict-free scalar stores.
-//  * Thread 0 issues the MMAs (tcgen05.mma.cta_group::1.kind::tf32) and
-//    commits each slot to an mbarrier; staging of chunk c+1 overlaps the MMAs
-//    of chunk c.
+//    pre-laid-out weight chunk brought in by a TMA bulk copy from an
+//    L2-resident image (tc_prep_kernel builds it once per step).
+//    Weight-gradient GEMMs (K = samples, one quadrant's 32 rows per chunk)
+//    use MN-major SWIZZLE_128B_BASE32B tiles written as float4s by the
+//    sample's thread (hidden layers: dW^T = X^T G); layer 0 uses 128B-swizzled
+//    K-major transposed tiles.
+//  * Warps 0-7 (two per TMEM lane quadrant, 64 columns each) stage, run the
+//    epilogues and the render chain; warp 8 lane 0 issues the MMAs
+//    (tcgen05.mma.cta_group::1.kind::tf32) from an smem schedule table and
+//    commits each slot / GEMM to mbarriers, so staging of later chunks
+//    overlaps the MMAs of earlier ones.
 //  * Weight gradients leave through TMEM -> registers -> the CTA's partial
 //    gradient block; bias gradients are warp butterfly reductions; the
 //    per-model sum over tiles is reduce_partials_kernel (fixed order).

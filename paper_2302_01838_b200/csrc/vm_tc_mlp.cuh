@@ -60,7 +60,6 @@ constexpr int kNS = 3;         // ring slots
 constexpr int kSlot = 65536;   // bytes per slot: A (32 KB) | B (32 KB)
 constexpr int kHalfSlot = 32768;
 constexpr int kK0 = 40;        // layer-0 fan-in padded for the MMA (33 -> 40)
-constexpr int kN0 = 48;        // layer-0 fan-in rows of X0^T for dW0 (N % 16)
 
 // Pre-split weight image (floats) per model: chunks of [H rows][kw cols]
 // (hi tile then lo tile, interleaved layout), forward W_l (rows = fo, K = fi)
@@ -247,7 +246,7 @@ __device__ __forceinline__ void for_each_chunk(F&& f) {
       f(j++, Chunk{0, 32, 4, H, 0, c == 0, c == H / 32 - 1, I::fwd_off(l) + c * I::kC32, I::kC32});
   for (int c = 0; c < 4; ++c) f(j++, Chunk{2, 32, 4, 16, H, c == 0, c == 3, -1, 0});
   for (int l = L - 2; l >= 0; --l) {
-    for (int c = 0; c < 4; ++c) f(j++, Chunk{l == 0 ? 1 : 2, 32, 4, l == 0 ? kN0 : H, H, c == 0, c == 3, -1, 0});
+    for (int c = 0; c < 4; ++c) f(j++, Chunk{2, 32, 4, H, H, c == 0, c == 3, -1, 0});
     if (l > 0)
       for (int c = 0; c < H / 32; ++c)
         f(j++, Chunk{0, 32, 4, H, 0, c == 0, c == H / 32 - 1, I::dx_off(l) + c * I::kC32, I::kC32});
@@ -461,16 +460,6 @@ __global__ void __launch_bounds__(kTCThreads, 1)
       }
     };
     // element (tile row i, sample lane) of a transposed 128B-swizzled hi/lo tile
-    uint32_t swo[8];  // per-lane byte offset within a 128-B row for row % 8
-#pragma unroll
-    for (int r8 = 0; r8 < 8; ++r8) swo[r8] = sw128_off(r8, lane);
-    auto put_t = [&](uint8_t* t, int rows, int i, float v) {
-      float a, b;
-      split_fast(v, a, b);
-      const uint32_t o = uint32_t(i >> 3) * 1024u + swo[i & 7];
-      *reinterpret_cast<float*>(t + o) = a;
-      *reinterpret_cast<float*>(t + rows * 128 + o) = b;
-    };
     // 32 features [f0, f0+32) of this lane's sample into an MN-major hi/lo tile
     auto put_mn = [&](uint8_t* t, int f0, const float (&v)[32]) {
 #pragma unroll
@@ -736,27 +725,34 @@ __global__ void __launch_bounds__(kTCThreads, 1)
       for (int c = 0; c < 4; ++c) {
         uint8_t* sl = acquire();
         if (q == c) {
-          uint8_t* gt = (l == 0) ? sl : sl + kHalfSlot;  // G tile
-          uint8_t* xt = (l == 0) ? sl + kHalfSlot : sl;  // X tile
+          uint8_t* gt = sl + kHalfSlot;  // B = G_l (N = fan-out)
+          uint8_t* xt = sl;              // A = X_l (M = fan-in; layer 0 zero-padded to 128)
           float gv2[2][32];
           ld64(R(l + 1) + c0, R(l + 1) + c0 + 32, gv2[0], gv2[1]);
 #pragma unroll
           for (int g = 0; g < 2; ++g) {
             float (&v)[32] = gv2[g];
-            if (l == 0) {
-#pragma unroll
-              for (int j = 0; j < 32; ++j) put_t(gt, H, c0 + 32 * g + j, v[j]);
-            } else {
-              put_mn(gt, c0 + 32 * g, v);
-            }
+            put_mn(gt, c0 + 32 * g, v);
             myDb[l * H + c0 + 32 * g + lane] += warp_colsum(v);
           }
           if (l == 0) {
-            float x0[kK0];
-            input_row(st, sCoef, gs0 + row, row < ns, x0);
+            // layer-0 input recomputed (positional encoding), features
+            // 40..127 are zero padding so M = 128
+            float xa[32], xb[32];
+            if (h == 0) {
+              float x0[kK0];
+              input_row(st, sCoef, gs0 + row, row < ns, x0);
 #pragma unroll
-            for (int i = 0; i < kN0; ++i)
-              if (i / (kN0 / 2) == h) put_t(xt, kN0, i, i < kK0 ? x0[i < kK0 ? i : 0] : 0.f);
+              for (int i = 0; i < 32; ++i) {
+                xa[i] = x0[i];
+                xb[i] = (32 + i < kK0) ? x0[32 + i < kK0 ? 32 + i : 0] : 0.f;
+              }
+            } else {
+#pragma unroll
+              for (int i = 0; i < 32; ++i) xa[i] = xb[i] = 0.f;
+            }
+            put_mn(xt, c0, xa);
+            put_mn(xt, c0 + 32, xb);
           } else {
             float xv[2][32];
             ld64(R(l) + c0, R(l) + c0 + 32, xv[0], xv[1]);
@@ -767,27 +763,18 @@ __global__ void __launch_bounds__(kTCThreads, 1)
         release();
       }
       wait_acc();
-      if (l > 0) {  // drain dW_l^T: lane = fan-in i, columns = this half's fan-out rows
+      {  // drain dW_l^T: lane = fan-in i, columns = this half's fan-out rows
         const int i = row;
+        const int fi_pad = (l == 0) ? st.fi0 : H;  // layer 0: fan-in rows >= 36 do not exist
         float* dst = gdst + st.w_off[l] + i;
 #pragma unroll
         for (int cc = 0; cc < HC; cc += 16) {
           float v[16];
-          tc::tmem_ld16(R(0) + c0 + cc, v);
+          tc::tmem_ld16(R(0) + c0 + cc, v);  // warp-wide (.sync.aligned): no divergence before it
+          if (i < fi_pad) {
 #pragma unroll
-          for (int j = 0; j < 16; ++j) dst[(c0 + cc + j) * H] = v[j];
-        }
-      } else {  // drain dW_0 (lane = fan-out row; this half's fan-in columns)
-        const int o = row;
-        const int fi_pad = st.fi0;
-        const int cb = h * (kN0 / 2);
-        float* dst = gdst + st.w_off[0] + o * fi_pad;
-        for (int cc = 0; cc < kN0 / 2; cc += 8) {
-          float v[16];
-          tc::tmem_ld16(R(0) + cb + cc, v);
-#pragma unroll
-          for (int j = 0; j < 8; ++j)
-            if (cb + cc + j < fi_pad) dst[cb + cc + j] = v[j];
+            for (int j = 0; j < 16; ++j) dst[(c0 + cc + j) * fi_pad] = v[j];
+          }
         }
       }
       if (l == 0) break;

@@ -253,6 +253,12 @@ def main():
     n_launch = C.c_int()
     mlp_ms = C.c_double()
     lib.vm_profile_read(C.byref(n_launch), C.byref(mlp_ms))
+    # our kernels per graph-replayed step: those the eager steps launched
+    # (vm_train_step + vm_sample count their launches) + the step-counter bump
+    n_eager = C.c_long()
+    lib.vm_profile_kernels(C.byref(n_eager))
+    if n_eager.value > 0:
+        kernels_per_step = n_eager.value // n_prof + 1
     per_tag = {}
     for tag in (1, 2, 3):  # 1: FFMA kernel KF (objects), 2: tensor-core branch KT (background), 3: reduce + Adam
         n_t, ms_t = C.c_int(), C.c_double()

@@ -16,7 +16,10 @@
  *   - Return codes: VM_OK, VM_ERR_SHAPE (bad arguments), VM_ERR_CUDA (launch
  *     error; see vm_last_error()), VM_ERR_UNSUPPORTED (arch outside the
  *     compiled kernel set).
- *   - Not reentrant per stack (single writer).
+ *   - Not reentrant per stack (single writer).  Different host
+ *     threads may drive different stacks/devices concurrently: the library's
+ *     internal side stream and fork/join events (vm_train_step's tensor-core
+ *     branch) are per (host thread, device).
  *
  * Parameter storage: one model-major arena per stack,
  *   arena[capacity][block],  block = sum over layers of (fo_pad*fi_pad + fo_pad)
@@ -41,7 +44,7 @@ extern "C" {
 #define VM_ERR_UNSUPPORTED 4
 
 #define VM_MAX_LAYERS 8
-#define VM_MAX_STACKS 4
+#define VM_MAX_STACKS 2
 
 /* models.py:19-55 ModelArch (output_dim is always 4: occupancy + RGB). */
 typedef struct VmArch {
@@ -73,13 +76,15 @@ typedef struct VmStack {
   int64_t* step;          /* [capacity] Adam step counters */
   const uint8_t* frozen;  /* [capacity] */
   /* Bias corrections f32(1 - beta^t) computed in f64 on the host exactly as
-     models.py:434-436 does; index t-1.  For t > corr_len both are 1.0f. */
+     models.py:434-436 does; index t-1.  For t > corr_len the device computes
+     f32(1 - pow(beta, t)) in f64 from beta1/beta2 below. */
   const float* corr1;
   const float* corr2;
   int32_t corr_len;
   /* f32 constants as numpy forms them (models.py:444-457):
      beta1f = f32(b1), omb1 = f32(1-b1), beta2f, omb2 = f32(1-b2), eps, lr. */
   float beta1f, omb1, beta2f, omb2, eps, lr;
+  double beta1, beta2;    /* the python-float betas (bias corrections past corr_len) */
 } VmStack;
 
 /* RaySampleBatch (trainer.py:162-173), stacked on a leading model axis.

@@ -39,7 +39,7 @@ class VmStack(C.Structure):
                 ("frozen", C.c_void_p), ("corr1", C.c_void_p), ("corr2", C.c_void_p),
                 ("corr_len", C.c_int32),
                 ("beta1f", C.c_float), ("omb1", C.c_float), ("beta2f", C.c_float), ("omb2", C.c_float),
-                ("eps", C.c_float), ("lr", C.c_float)]
+                ("eps", C.c_float), ("lr", C.c_float), ("beta1", C.c_double), ("beta2", C.c_double)]
 
 
 class VmBatch(C.Structure):
@@ -122,7 +122,7 @@ def load(path: Path | None = None) -> C.CDLL:
     global _lib
     if _lib is not None:
         return _lib
-    p = Path(path) if path else LIB_PATH
+    p = Path(path) if path else Path(os.environ.get("VM_LIB", LIB_PATH))  # VM_LIB: A/B builds (scripts)
     if not p.exists():
         raise RuntimeError(
             f"libvmap_b200.so not found at {p}; build it with `python -c "

@@ -14,7 +14,17 @@ struct AdamConsts {
   const float* corr1;
   const float* corr2;
   int corr_len;
+  double beta1, beta2;
 };
+
+// f32(1 - beta^t) for t = step + 1 (models.py:434-436): the host's f64 table
+// for t <= corr_len, else the same f64 expression on the device.
+__device__ __forceinline__ float2 bias_corrections(const float* corr1, const float* corr2, int corr_len, double b1,
+                                                   double b2, int64_t step) {
+  const int64_t t = step + 1;
+  if (t <= corr_len) return make_float2(corr1[t - 1], corr2[t - 1]);
+  return make_float2(float(1.0 - pow(b1, double(t))), float(1.0 - pow(b2, double(t))));
+}
 
 __device__ __forceinline__ void adam_elem(float& p, float& m, float& v, float g, float c1, float c2,
                                           const AdamConsts& a) {
@@ -32,14 +42,9 @@ __device__ __forceinline__ void adam_elem(float& p, float& m, float& v, float g,
 }
 
 __device__ __forceinline__ void adam_corr(const AdamConsts& a, int64_t step, float& c1, float& c2) {
-  const int64_t t = step + 1;
-  if (t <= a.corr_len) {
-    c1 = a.corr1[t - 1];
-    c2 = a.corr2[t - 1];
-  } else {
-    c1 = 1.0f;
-    c2 = 1.0f;
-  }
+  const float2 c = bias_corrections(a.corr1, a.corr2, a.corr_len, a.beta1, a.beta2, step);
+  c1 = c.x;
+  c2 = c.y;
 }
 
 // One float4 of model `k`'s block.  Caller guarantees the model is active.
@@ -58,7 +63,7 @@ __device__ __forceinline__ void adam_vec4(float* __restrict__ P, float* __restri
 }
 
 inline AdamConsts adam_consts(const VmStack& s) {
-  return AdamConsts{s.beta1f, s.omb1, s.beta2f, s.omb2, s.eps, s.lr, s.corr1, s.corr2, s.corr_len};
+  return AdamConsts{s.beta1f, s.omb1, s.beta2f, s.omb2, s.eps, s.lr, s.corr1, s.corr2, s.corr_len, s.beta1, s.beta2};
 }
 
 }  // namespace vm

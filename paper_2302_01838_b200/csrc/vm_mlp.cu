@@ -77,78 +77,6 @@ __device__ __forceinline__ void load_block(const KStack& st, int k, int64_t gs0,
   if (with_t && tt < kSB) tS[tt] = tt < ns ? st.t[gs0 + tt] : 0.f;
 }
 
-// Per-model epilogue of a training step: update mask = ray_ok.any(-1)
-// (trainer.py:504) and active = !frozen; the model's loss triple as numpy's
-// pairwise sum over rays of the per-ray terms (render.py:305-307); the
-// non-finite flags Adam and the host need (models.py:423-428,
-// trainer.py:404-407); this step's bias corrections.  Called by all threads
-// of a CTA.  `meta` selects the writer of the per-model words.
-__device__ void finalize_model(const KStack& st, int k, bool all_finite, bool meta, float* scratch,
-                               int scratch_floats) {
-  const int tid = threadIdx.x;
-  // non-meta CTAs only need the update mask when their chunk is non-finite
-  // (both conditions are CTA-uniform, so the barrier below is too)
-  if (!meta && all_finite) return;
-  bool any_ok = false;
-  for (int r = tid; r < st.R; r += blockDim.x) any_ok |= st.ok[int64_t(k) * st.R + r] != 0;
-  const bool upd = __syncthreads_or(any_ok);
-  const bool active = upd && !st.frozen[k];
-  if (tid == 0 && active && !all_finite) atomicMin(&st.status[0], k);
-  if (!meta) return;
-  // stage the per-ray terms in smem (coalesced), then 3 threads sum them in
-  // numpy's pairwise order without a global-load latency per add
-  const float* terms = st.ray_terms + int64_t(k) * st.R * 3;
-  const bool staged = st.R * 3 <= scratch_floats;
-  if (staged) {
-    for (int i = tid; i < st.R * 3; i += blockDim.x) scratch[i] = __ldcg(terms + i);
-    __syncthreads();
-  }
-  // more than one pairwise leaf: the leaves (<= 128 rays each) are summed by
-  // separate threads, then combined in the recursion's order (same bits)
-  constexpr int kMaxLeaves = 64;
-  __shared__ int64_t lf_start[kMaxLeaves];
-  __shared__ int lf_len[kMaxLeaves];
-  __shared__ float lf_sum[3][kMaxLeaves];
-  __shared__ int lf_n;
-  const bool parallel = staged && st.R > 128 && 3 * kMaxLeaves <= int(blockDim.x);
-  if (parallel) {
-    if (tid == 0) lf_n = pairwise_leaves(st.R, lf_start, lf_len, kMaxLeaves);
-    __syncthreads();
-  }
-  if (parallel && lf_n <= kMaxLeaves) {
-    if (tid < 3 * lf_n) {
-      const int j = tid % 3, lf = tid / 3;
-      lf_sum[j][lf] = pairwise_sum_leaf([&](int64_t r) { return scratch[r * 3 + j]; }, lf_start[lf], lf_len[lf]);
-    }
-    __syncthreads();
-    if (tid < 3) {
-      int next = 0;
-      const float sum = pairwise_combine(st.R, lf_sum[tid], next);
-      st.losses[int64_t(k) * 3 + tid] = sum;
-      if (!isfinite(sum)) atomicMin(&st.status[1], k);
-    }
-  } else if (tid < 3) {
-    const int j = tid;
-    const float sum = staged ? pairwise_sum([&](int64_t r) { return scratch[r * 3 + j]; }, st.R)
-                             : pairwise_sum([&](int64_t r) { return __ldcg(terms + r * 3 + j); }, st.R);
-    st.losses[int64_t(k) * 3 + j] = sum;
-    if (!isfinite(sum)) atomicMin(&st.status[1], k);
-  }
-  if (tid == 0) {
-    st.upd[k] = active ? 1 : 0;
-    const int64_t t = st.step[k] + 1;
-    float2 c;
-    if (t <= st.corr_len) {
-      c.x = st.corr1[t - 1];
-      c.y = st.corr2[t - 1];
-    } else {
-      c.x = 1.0f;
-      c.y = 1.0f;
-    }
-    st.corr[k] = c;
-  }
-}
-
 }  // namespace vm
 
 #include "vm_tc_mlp.cuh"
@@ -511,15 +439,38 @@ __device__ void run_item(const KStack& st, int item, float* smem) {
   }
 
   // ---------------- per-model finalisation ---------
-  // Split models (P > 1) are reduced and finalised by reduce_partials_kernel;
-  // a single-CTA model finishes here.
-  if (st.P > 1) return;
-  __syncthreads();
-  const float* gk = st.grads + int64_t(k) * st.block;
+  // A model split over P CTAs (fixed chunks of its own blocks, so the split
+  // never depends on K) is summed by the CTA that finishes last (atomic
+  // ticket), partials in chunk order -- deterministic and identical for the
+  // vectorised and the sequential paths -- then finalised right here.
   bool finite = true;
-  for (int i = tid; i < st.block / 4; i += kThreads) {
-    const float4 v = ld4(gk + 4 * i);
-    finite &= isfinite(v.x) && isfinite(v.y) && isfinite(v.z) && isfinite(v.w);
+  const float* gk = st.grads + int64_t(k) * st.block;
+  if (st.P > 1) {
+    __shared__ int s_last;
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) s_last = atomicAdd(&st.counters[k], 1) == st.P - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    const float* pb = st.partials + int64_t(k) * st.P * st.block;
+    float* gw = st.grads + int64_t(k) * st.block;
+    for (int i = tid; i < st.block / 4; i += kThreads) {
+      float4 v = __ldcg(reinterpret_cast<const float4*>(pb + 4 * i));
+      for (int u = 1; u < st.P; ++u) {
+        const float4 w = __ldcg(reinterpret_cast<const float4*>(pb + int64_t(u) * st.block + 4 * i));
+        v.x += w.x; v.y += w.y; v.z += w.z; v.w += w.w;
+      }
+      st4(gw + 4 * i, v);
+      finite &= isfinite(v.x) && isfinite(v.y) && isfinite(v.z) && isfinite(v.w);
+    }
+    if (tid == 0) st.counters[k] = 0;  // ready for the next launch (graph replay)
+  } else {
+    __syncthreads();
+    for (int i = tid; i < st.block / 4; i += kThreads) {
+      const float4 v = ld4(gk + 4 * i);
+      finite &= isfinite(v.x) && isfinite(v.y) && isfinite(v.z) && isfinite(v.w);
+    }
   }
   const bool all_finite = __syncthreads_and(finite);
   if (MODE == kBackward) return;
@@ -528,7 +479,7 @@ __device__ void run_item(const KStack& st, int item, float* smem) {
 }
 
 template <int H0, int L0, int H1, int L1, int MODE>
-__global__ void __launch_bounds__(kThreads, 1) mlp_kernel(const __grid_constant__ KParams p) {
+__global__ void __launch_bounds__(kThreads, (H0 <= 32 && H1 <= 32) ? 2 : 1) mlp_kernel(const __grid_constant__ KParams p) {
   extern __shared__ __align__(16) float smem[];
   const int b = blockIdx.x;
   if (p.n_stacks == 1 || b < p.s[1].item_base) {
@@ -583,7 +534,7 @@ struct Instance {
 };
 
 inline size_t smem_bytes(const KStack& s) {
-  const int nteams = kWarps / (s.H == 32 ? 1 : (s.H == 64 ? 4 : 8));
+  const int nteams = kWarps / (s.H == 32 ? TeamCfg<32>::T : (s.H == 64 ? TeamCfg<64>::T : TeamCfg<128>::T));
   return size_t(s.w_floats + nteams * s.team_floats) * sizeof(float) + 64;
 }
 
@@ -610,6 +561,8 @@ static int fill_stack(const VmStack& vs, KStack& ks, VmLayout& L) {
   ks.corr1 = vs.corr1;
   ks.corr2 = vs.corr2;
   ks.corr_len = vs.corr_len;
+  ks.beta1 = vs.beta1;
+  ks.beta2 = vs.beta2;
   ks.K = vs.count;
   return VM_OK;
 }
@@ -645,52 +598,32 @@ static int launch_mlp(KernelFn fn, const KParams& p, int grid, size_t smem, cuda
   return VM_OK;
 }
 
-// Work split: CTAs per model from the model's own cost only (never from K),
-// so a model's gradient summation order -- and therefore its bits -- does
+// Work split: a model's ray blocks are cut into fixed chunks of
+// VM_KF_CHUNK blocks (default 8: two per 2-warp team of a CTA), one CTA per
+// chunk.  The chunking depends only on the model's own ray count, never on
+// K, so a model's gradient summation order -- and therefore its bits -- does
 // not depend on which other models share the launch (vectorised ==
-// sequential, test_trainer.py:117-132).  One CTA per ~7 MFLOP of work
-// (VM_SPLIT_MFLOP overrides): a 120-ray hidden-32 object is three CTAs; a
-// tensor-core stack is one CTA per 128-row tile instead (choose_splits).
-double target_flop() {
-  static const double v = [] {
-    const char* e = std::getenv("VM_SPLIT_MFLOP");
-    return (e ? std::atof(e) : 7.0) * 1e6;
+// sequential, test_trainer.py:117-132), while the grid is a few hundred small
+// CTAs that the block scheduler spreads over all 148 SMs (two per SM) and
+// that fill the SMs the tensor-core kernel leaves free.  A tensor-core stack
+// is one CTA per 128-row tile instead.
+int chunk_blocks() {
+  static const int v = [] {
+    const char* e = std::getenv("VM_KF_CHUNK");
+    const int c = e ? std::atoi(e) : 8;
+    return c > 0 ? c : 8;
   }();
   return v;
 }
-constexpr int kSMs = 148;
-
-static int blocks_per_split(int nblk, int p) {
-  p = std::max(1, std::min(p, nblk));
-  return (nblk + p - 1) / p;
-}
-
 static int choose_splits(const KStack* ks, int n, int* P) {
-  int nblk[2], total = 0;
   for (int i = 0; i < n; ++i) {
     if (ks[i].tc) {
       const int g = tck::kTM / ks[i].S;
       P[i] = std::max(1, (ks[i].R + g - 1) / g);
-      nblk[i] = 0;
       continue;
     }
-    const double flop_per_sample = double(ks[i].H) * (ks[i].Dp + 2 * (ks[i].L - 2) * ks[i].H + 8) * 3.0;
-    const double cost = flop_per_sample * ks[i].R * ks[i].S;
-    nblk[i] = (ks[i].R + ks[i].G - 1) / ks[i].G;
-    const int bps = blocks_per_split(nblk[i], int(cost / target_flop() + 0.5));
-    P[i] = (nblk[i] + bps - 1) / bps;  // drop empty CTAs
-    total += ks[i].K * P[i];
-  }
-  // Keep a multi-stack launch within one wave of 148 SMs: a second wave of a
-  // few CTAs doubles the kernel time.  Shrink the most-split stack to fit.
-  if (n > 1 && total > kSMs && !ks[0].tc && !ks[1].tc) {
-    int big = ks[0].K * P[0] >= ks[1].K * P[1] ? 0 : 1;
-    const int others = total - ks[big].K * P[big];
-    const int budget = (kSMs - others) / std::max(1, ks[big].K);
-    if (budget >= 1 && P[big] > 1) {
-      const int bps = blocks_per_split(nblk[big], budget);
-      P[big] = (nblk[big] + bps - 1) / bps;
-    }
+    const int nblk = (ks[i].R + ks[i].G - 1) / ks[i].G;
+    P[i] = std::max(1, (nblk + chunk_blocks() - 1) / chunk_blocks());
   }
   return VM_OK;
 }
@@ -736,6 +669,16 @@ struct TrainPlan {
 };
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// The specialised hidden-32 kernel (vm_kf32.cu) is the default for the
+// object stacks; VM_KF32=0 selects the generic FFMA kernel (A/B, parity).
+bool kf32_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("VM_KF32");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
 
 // The tensor-core path is the default for hidden-128 stacks; VM_TC=0 selects
 // the FFMA kernel for them (A/B measurements and the parity cross-check).
@@ -825,7 +768,7 @@ int plan_train(const VmStack* stacks, const VmBatch* batches, int n, TrainPlan& 
 int reduce_and_adam(const TrainPlan& pl, int n_stacks, int first, int last, cudaStream_t s) {
   for (int i = first; i < last; ++i) {
     const KStack& ks = pl.kp.s[i];
-    if (ks.P <= 1 || ks.K == 0) continue;
+    if (ks.P <= 1 || ks.K == 0 || !ks.tc) continue;  // FFMA stacks reduce in-kernel
     const int cf = red_chunk_floats(ks.P);
     const int grid = ks.K * ((ks.block + cf - 1) / cf);
     const int red_smem = ks.R * 3 * 4;
@@ -862,6 +805,11 @@ extern "C" int vm_train_step(const VmStack* stacks, const VmBatch* batches, int 
   cudaStream_t s = cudaStream_t(stream);
   char* ws = static_cast<char*>(workspace);
   VM_CUDA(cudaMemsetAsync(status, 0x7f, sizeof(int32_t) * 4 * n_stacks, s));
+  // chunk tickets of the in-kernel partial reduction (the workspace may have
+  // held another plan's data)
+  for (int i = 0; i < n_stacks; ++i)
+    if (!pl.kp.s[i].tc && pl.kp.s[i].P > 1 && pl.kp.s[i].K > 0)
+      VM_CUDA(cudaMemsetAsync(ws + pl.off_cnt[i], 0, sizeof(int) * pl.kp.s[i].K, s));
   int loss_off = 0;
   for (int i = 0; i < n_stacks; ++i) {
     KStack& ks = pl.kp.s[i];
@@ -895,10 +843,11 @@ extern "C" int vm_train_step(const VmStack* stacks, const VmBatch* batches, int 
     kf.n_stacks++;
   }
   KernelFn fn = nullptr;
-  if (kf.n_stacks > 0) {
+  const bool use_kf32 = kf.n_stacks > 0 && kf32_enabled() && kf32_supported(kf);
+  if (kf.n_stacks > 0 && !use_kf32) {
     fn = pick_kernel<kTrain>(kf.s[0].H, kf.s[0].L, kf.n_stacks > 1 ? kf.s[1].H : 0, kf.n_stacks > 1 ? kf.s[1].L : 0);
   }
-  if (kf.n_stacks > 0 && !fn) {
+  if (kf.n_stacks > 0 && !fn && !use_kf32) {
     if (n_stacks == 2) {  // no fused instantiation for this pair: run stacks back to back
       // (Adam of stack 1 still honours stack 0's status because both read it)
       set_error("vm_train_step: unsupported stack pair");
@@ -917,8 +866,19 @@ extern "C" int vm_train_step(const VmStack* stacks, const VmBatch* batches, int 
   // Their weight images are built on `s` before the fork; the FFMA kernel is
   // launched right after the fork, then KT, whose one-tile-per-SM CTAs take
   // the SMs the first FFMA wave leaves and those it frees.
-  static cudaStream_t side = nullptr;
-  static cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  // side stream + fork/join events: one set per (host thread, device), so
+  // concurrent callers on different threads or devices never share them
+  struct SideRes {
+    cudaStream_t side = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
+  };
+  static thread_local SideRes side_res[64];
+  int dev = 0;
+  VM_CUDA(cudaGetDevice(&dev));
+  VM_REQUIRE(dev >= 0 && dev < 64, "vm_train_step: device ordinal out of range");
+  cudaStream_t& side = side_res[dev].side;
+  cudaEvent_t& ev_fork = side_res[dev].fork;
+  cudaEvent_t& ev_join = side_res[dev].join;
   bool forked = false;
   cudaStream_t ts = s;
   using TI = tck::Img<128, 4>;
@@ -931,12 +891,12 @@ extern "C" int vm_train_step(const VmStack* stacks, const VmBatch* batches, int 
     if (g_prof.on) g_prof.kernels += 1;
   }
   auto launch_kf = [&]() -> int {
-    if (!fn) return VM_OK;
+    if (!fn && !use_kf32) return VM_OK;
     if (g_prof.on) {
       g_prof.pair(kf0, kf1, 1);
       VM_CUDA(cudaEventRecord(kf0, s));
     }
-    const int r = launch_mlp(fn, kf, ff_grid, pl.smem, s);
+    const int r = use_kf32 ? launch_kf32(kf, ff_grid, s) : launch_mlp(fn, kf, ff_grid, pl.smem, s);
     if (r) return r;
     if (g_prof.on) {
       g_prof.kernels += 1;
@@ -958,7 +918,7 @@ extern "C" int vm_train_step(const VmStack* stacks, const VmBatch* batches, int 
       const char* e = std::getenv("VM_NO_FORK");
       return e && e[0] == '1';
     }();
-    if (!forked && fn && !no_fork) {
+    if (!forked && (fn || use_kf32) && !no_fork) {
       if (!side) {  // first use may be inside a graph capture: relax the capture mode for the creation
         cudaStreamCaptureMode mode = cudaStreamCaptureModeRelaxed;
         VM_CUDA(cudaThreadExchangeStreamCaptureMode(&mode));

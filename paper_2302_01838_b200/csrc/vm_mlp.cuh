@@ -41,7 +41,10 @@ constexpr int kLD = 36;    // activation row stride in floats (== 4 mod 32)
 constexpr int kDpMax = 40; // max padded input rows
 
 template <int H> struct TeamCfg;
-template <> struct TeamCfg<32> { static constexpr int T = 1, OW = 32; };
+// hidden 32: teams of 2 warps (16 outputs each) so a warp's share of the
+// register-resident weight gradient is ~58 floats and two 8-warp CTAs fit an
+// SM (16 warps; 128 registers, ~92 KB smem each).
+template <> struct TeamCfg<32> { static constexpr int T = 2, OW = 16; };
 template <> struct TeamCfg<64> { static constexpr int T = 4, OW = 16; };
 template <> struct TeamCfg<128> { static constexpr int T = 8, OW = 16; };
 
@@ -62,6 +65,7 @@ struct KStack {
   const float* corr1;
   const float* corr2;
   int corr_len;
+  double beta1, beta2;
   const float* enc;       // [K][R*S][D] encoded samples, or
   const float* pts;       // [K][R*S][3] box-normalised points (PE fused here)
   const float* pe_scale;  // [K] per-model PE scale (points path)
@@ -91,6 +95,11 @@ struct KParams {
   KStack s[2];
   int n_stacks;
 };
+
+// vm_kf32.cu: the specialised hidden-32 / 4-layer train kernel
+bool kf32_supported(const KParams& p);
+size_t kf32_smem_bytes();
+int launch_kf32(const KParams& p, int grid, cudaStream_t s);
 
 __device__ __forceinline__ void team_sync(int team, int T) {
   if (T == 1) {
@@ -301,5 +310,69 @@ struct WarpGrads {
     bl = 0.f;
   }
 };
+
+// Per-model epilogue of a training step: update mask = ray_ok.any(-1)
+// (trainer.py:504) and active = !frozen; the model's loss triple as numpy's
+// pairwise sum over rays of the per-ray terms (render.py:305-307); the
+// non-finite flags Adam and the host need (models.py:423-428,
+// trainer.py:404-407); this step's bias corrections.  Called by all threads
+// of a CTA.  `meta` selects the writer of the per-model words.
+__device__ inline void finalize_model(const KStack& st, int k, bool all_finite, bool meta, float* scratch,
+                               int scratch_floats) {
+  const int tid = threadIdx.x;
+  // non-meta CTAs only need the update mask when their chunk is non-finite
+  // (both conditions are CTA-uniform, so the barrier below is too)
+  if (!meta && all_finite) return;
+  bool any_ok = false;
+  for (int r = tid; r < st.R; r += blockDim.x) any_ok |= st.ok[int64_t(k) * st.R + r] != 0;
+  const bool upd = __syncthreads_or(any_ok);
+  const bool active = upd && !st.frozen[k];
+  if (tid == 0 && active && !all_finite) atomicMin(&st.status[0], k);
+  if (!meta) return;
+  // stage the per-ray terms in smem (coalesced), then 3 threads sum them in
+  // numpy's pairwise order without a global-load latency per add
+  const float* terms = st.ray_terms + int64_t(k) * st.R * 3;
+  const bool staged = st.R * 3 <= scratch_floats;
+  if (staged) {
+    for (int i = tid; i < st.R * 3; i += blockDim.x) scratch[i] = __ldcg(terms + i);
+    __syncthreads();
+  }
+  // more than one pairwise leaf: the leaves (<= 128 rays each) are summed by
+  // separate threads, then combined in the recursion's order (same bits)
+  constexpr int kMaxLeaves = 64;
+  __shared__ int64_t lf_start[kMaxLeaves];
+  __shared__ int lf_len[kMaxLeaves];
+  __shared__ float lf_sum[3][kMaxLeaves];
+  __shared__ int lf_n;
+  const bool parallel = staged && st.R > 128 && 3 * kMaxLeaves <= int(blockDim.x);
+  if (parallel) {
+    if (tid == 0) lf_n = pairwise_leaves(st.R, lf_start, lf_len, kMaxLeaves);
+    __syncthreads();
+  }
+  if (parallel && lf_n <= kMaxLeaves) {
+    if (tid < 3 * lf_n) {
+      const int j = tid % 3, lf = tid / 3;
+      lf_sum[j][lf] = pairwise_sum_leaf([&](int64_t r) { return scratch[r * 3 + j]; }, lf_start[lf], lf_len[lf]);
+    }
+    __syncthreads();
+    if (tid < 3) {
+      int next = 0;
+      const float sum = pairwise_combine(st.R, lf_sum[tid], next);
+      st.losses[int64_t(k) * 3 + tid] = sum;
+      if (!isfinite(sum)) atomicMin(&st.status[1], k);
+    }
+  } else if (tid < 3) {
+    const int j = tid;
+    const float sum = staged ? pairwise_sum([&](int64_t r) { return scratch[r * 3 + j]; }, st.R)
+                             : pairwise_sum([&](int64_t r) { return __ldcg(terms + r * 3 + j); }, st.R);
+    st.losses[int64_t(k) * 3 + j] = sum;
+    if (!isfinite(sum)) atomicMin(&st.status[1], k);
+  }
+  if (tid == 0) {
+    st.upd[k] = active ? 1 : 0;
+    st.corr[k] = bias_corrections(st.corr1, st.corr2, st.corr_len, st.beta1, st.beta2, st.step[k]);
+  }
+}
+
 
 }  // namespace vm

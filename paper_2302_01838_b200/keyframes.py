@@ -86,6 +86,7 @@ class DeviceTable:
         self.device = device
         self.buf = None
         self.pinned = None
+        self.done = None   # event after the last staging copy
 
     def upload(self, raw: bytes) -> torch.Tensor:
         n = len(raw)
@@ -93,8 +94,14 @@ class DeviceTable:
             cap = max(256, 1 << (n - 1).bit_length())
             self.buf = torch.zeros(cap, dtype=torch.uint8, device=self.device)
             self.pinned = torch.zeros(cap, dtype=torch.uint8, pin_memory=True)
+            self.done = None
+        if self.done is not None:
+            self.done.synchronize()  # the previous non-blocking copy still reads the staging buffer
         self.pinned[:n].numpy()[:] = np.frombuffer(raw, dtype=np.uint8)
         self.buf[:n].copy_(self.pinned[:n], non_blocking=True)
+        if self.done is None:
+            self.done = torch.cuda.Event()
+        self.done.record()
         return self.buf
 
 

@@ -61,6 +61,7 @@ class Mapper:
         self._dev_tables = [(DeviceTable(self.device), DeviceTable(self.device)) for _ in range(2)]
         self._dirty = True
         self._pin_scale = None
+        self._pin_done = None
         self._n_kf = 0
 
     # ------------------------------------------------------------ building
@@ -129,19 +130,32 @@ class Mapper:
         K = len(objs)
         if K and (self._buf_obj is None or self._buf_obj.K != K):
             self._buf_obj = SampleBuffers(K, c.rays_per_object, S, c.arch_object.input_dim, False, self.device)
+            self._g = None  # batch buffers reallocated: the step graphs must be recaptured
         if bg is not None and self._buf_bg is None:
             self._buf_bg = SampleBuffers(1, c.rays_background, S, c.arch_background.input_dim, False, self.device)
+            self._g = None
+        # frozen bits live in persistent device buffers the graphs read
+        if self.obj_params.count:
+            self.obj_params.frozen_device()
+        if self.bg_params.count:
+            self.bg_params.frozen_device()
         # PE scales through one pinned staging buffer (non-blocking uploads)
         sc = np.array([float(i.pe_scale) for i in objs] + ([float(bg.pe_scale)] if bg is not None else []),
                       np.float32)
         if self._pin_scale is None or self._pin_scale.numel() < max(len(sc), 1):
             self._pin_scale = torch.empty(max(len(sc), 64), dtype=torch.float32, pin_memory=True)
         if len(sc):
+            if self._pin_done is not None:
+                self._pin_done.synchronize()  # previous non-blocking upload still reads it
             self._pin_scale[:len(sc)].numpy()[:] = sc
         if K:
             self._buf_obj.pe_scale[:K].copy_(self._pin_scale[:K], non_blocking=True)
         if bg is not None:
             self._buf_bg.pe_scale[:1].copy_(self._pin_scale[K:K + 1], non_blocking=True)
+        if len(sc):
+            if self._pin_done is None:
+                self._pin_done = torch.cuda.Event()
+            self._pin_done.record()
         if self._g is not None:  # keep the graphs' second batch buffers' PE scales in step
             for a, b in zip(self._g["bufs"], (self._buf_obj, self._buf_bg)):
                 if a is not None and b is not None:
@@ -199,9 +213,16 @@ class Mapper:
 
     # ------------------------------------------------------------ graph replay
     def _graph_key(self):
+        """Everything a captured step graph bakes in: device pointers and the
+        model counts (grid sizes).  Keyframe counts, boxes, active and frozen
+        bits are NOT part of it -- they live in device tables refreshed in
+        place, so map growth at the steps_per_frame cadence replays the same
+        graphs (only arena or table reallocation forces a recapture)."""
         tabs = tuple(t.data_ptr() for tab in self._tables if tab is not None for t in tab)
         bufs = tuple(b.t.data_ptr() for b in (self._buf_obj, self._buf_bg) if b is not None)
-        return (self._sig, tabs, bufs, self.obj_params.arena.data_ptr(), self.bg_params.arena.data_ptr(),
+        frz = tuple(p.frozen_device().data_ptr() for p in (self.obj_params, self.bg_params) if p.count)
+        return (tabs, bufs, frz, self.arena.rgbd.data_ptr(), self.arena.mask.data_ptr(),
+                self.obj_params.arena.data_ptr(), self.bg_params.arena.data_ptr(),
                 self.obj_params.count, self.bg_params.count, self.cfg.train_background)
 
     def _build_graphs(self):

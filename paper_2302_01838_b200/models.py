@@ -139,10 +139,13 @@ class StackedModelParams:
 
     def frozen_device(self) -> torch.Tensor:
         """uint8 [capacity] device mirror of ``frozen`` (re-uploaded on change)."""
-        if (self._frozen_dev is None or self._frozen_dev.numel() != self.capacity
-                or not np.array_equal(self._frozen_seen, self.frozen)):
+        if self._frozen_dev is None or self._frozen_dev.numel() != self.capacity:
             self._frozen_seen = self.frozen.copy()
             self._frozen_dev = torch.from_numpy(self.frozen.astype(np.uint8)).to(self.arena.device)
+        elif not np.array_equal(self._frozen_seen, self.frozen):
+            # in place: captured step graphs keep reading the same buffer
+            self._frozen_seen = self.frozen.copy()
+            self._frozen_dev.copy_(torch.from_numpy(self.frozen.astype(np.uint8)))
         return self._frozen_dev
 
     def model_view(self, index: int) -> "StackedModelParams":
@@ -185,17 +188,30 @@ class OptimState:
     def corrections(self, device) -> tuple[torch.Tensor, torch.Tensor, int]:
         """f32(1 - beta**t) for t = 1..n computed in f64 like models.py:434-436.
 
-        Past n both are exactly 1.0f (0.9**t and 0.999**t fall below 2**-25).
+        The table runs until both corrections round to 1.0f (t = 165 / 17,330
+        for the default betas), capped at 2**18 entries; past the table the
+        kernels evaluate the same f64 expression with the device pow().
         """
         key = (self.beta1, self.beta2)
         if self._corr is None or self._corr[0] != key:
-            n = 32768
+            n = corrections_table_len(self.beta1, self.beta2)
             t = np.arange(1, n + 1, dtype=np.float64)
             c1 = (1.0 - self.beta1 ** t).astype(np.float32)
             c2 = (1.0 - self.beta2 ** t).astype(np.float32)
-            assert c1[-1] == 1.0 and c2[-1] == 1.0
             self._corr = (key, torch.from_numpy(c1).to(device), torch.from_numpy(c2).to(device), n)
         return self._corr[1], self._corr[2], self._corr[3]
+
+
+def corrections_table_len(beta1: float, beta2: float, cap: int = 1 << 18) -> int:
+    """Smallest power-of-two table length after which f32(1 - beta**t) == 1.0f
+    for both betas (models.py:434-436 arithmetic), at most `cap`."""
+    n = 1024
+    while n < cap:
+        t = np.float64(n)
+        if np.float32(1.0 - beta1 ** t) == 1.0 and np.float32(1.0 - beta2 ** t) == 1.0:
+            break
+        n *= 2
+    return min(n, cap)
 
 
 @dataclass
@@ -334,6 +350,7 @@ def vm_stack(params: StackedModelParams, state: OptimState | None = None) -> _li
         s.omb2 = float(f32(1.0 - state.beta2))
         s.eps = float(f32(state.eps))
         s.lr = float(f32(state.lr))
+        s.beta1, s.beta2 = float(state.beta1), float(state.beta2)
     return s
 
 

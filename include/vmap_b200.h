@@ -211,7 +211,7 @@ int vm_sample(const VmSampleObject* objects /* device [K] */, int n_objects,
 /* ---- profiling: event-time every fused-kernel launch of vm_train_step ---- */
 int vm_profile_enable(int on);                          /* resets the launch log */
 int vm_profile_read(int* launches, double* total_ms);   /* syncs on the events; MLP phase */
-/* tag: 0 = MLP phase (fork .. join), 1 = FFMA kernel KF, 2 = tensor-core branch KT, 3 = reduce + Adam */
+/* tag: 0 = MLP phase (fork .. join), 1 = FFMA kernel KF, 2 = tensor-core branch (KT + its partial reduce), 3 = Adam */
 int vm_profile_read_tag(int tag, int* launches, double* total_ms);
 int vm_profile_kernels(long* n);                        /* kernels launched since enable */
 void vm_profile_count_kernels(int n);                   /* internal: launch counter */

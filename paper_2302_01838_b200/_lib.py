@@ -122,7 +122,7 @@ def load(path: Path | None = None) -> C.CDLL:
     global _lib
     if _lib is not None:
         return _lib
-    p = Path(path) if path else Path(os.environ.get("VM_LIB", LIB_PATH))  # VM_LIB: A/B builds (scripts)
+    p = Path(path) if path else Path(os.environ.get("VM_LIB") or LIB_PATH)  # VM_LIB: A/B builds (scripts)
     if not p.exists():
         raise RuntimeError(
             f"libvmap_b200.so not found at {p}; build it with `python -c "

@@ -346,9 +346,22 @@ __global__ void __launch_bounds__(NTHR, 2) kf32_train_kernel(const __grid_consta
         if (wt == 1)
           for (int ff = st.D; ff < D0; ++ff) E[ff * kLD + s] = 0.f;
       } else {
-        const float* src = st.enc + (gs0 + s) * st.D;
-        const int f0 = wt == 0 ? 0 : (st.D + 1) / 2, f1 = wt == 0 ? (st.D + 1) / 2 : D0;
-        for (int ff = f0; ff < f1; ++ff) E[ff * kLD + s] = (s < ns && ff < st.D) ? src[ff] : 0.f;
+        // the block's ns x D encoded values are contiguous: coalesced loads
+        // by both warps, transposed into the feature-major tile
+        const int D = st.D, tt = wt * 32 + lane;
+        const float invD = 1.0f / float(D);
+        const float* src = st.enc + gs0 * D;
+        for (int idx = tt; idx < ns * D; idx += 64) {
+          const int ss = __float2int_rz((float(idx) + 0.5f) * invD), ff = idx - ss * D;
+          E[ff * kLD + ss] = __ldg(src + idx);
+        }
+        for (int idx = tt; idx < (D0 - D) * kSB; idx += 64) E[(D + idx / kSB) * kLD + (idx % kSB)] = 0.f;
+        const int np_ = kSB - ns;
+        if (np_ > 0)
+          for (int idx = tt; idx < np_ * D; idx += 64) {
+            const int ff = idx / np_;
+            E[ff * kLD + ns + (idx - ff * np_)] = 0.f;
+          }
       }
       if (wt == 0) tS[s] = s < ns ? st.t[gs0 + s] : 0.f;
       if (wt == 1 && s < nr) {  // this block's ray targets, read early (the render needs them mid-block)

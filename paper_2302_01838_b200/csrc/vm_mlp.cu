@@ -512,15 +512,34 @@ __global__ void __launch_bounds__(256) adam_train_kernel(const __grid_constant__
   if (p.n_stacks > 1 && b >= p.s[1].item_base) si = 1;
   const AdamStack& s = p.s[si];
   b -= s.item_base;
+  const int k = b / s.chunks, ch = b % s.chunks;
+  const int64_t base = int64_t(k) * s.block;
+  const int i = (ch * 256 + threadIdx.x) * 4;
+  // the element loads are issued before the (dependent) status / mask / bias
+  // correction reads, so one memory latency covers them all; nothing is
+  // written unless the model updates
+  const bool in = i < s.block;
+  float4 pv, mv, vv, gv;
+  if (in) {
+    pv = ld4(s.P + base + i);
+    mv = ld4(s.M + base + i);
+    vv = ld4(s.V + base + i);
+    gv = __ldcg(reinterpret_cast<const float4*>(s.G + base + i));
+  }
   bool skip = s.status[0] != 0x7f7f7f7f;
   for (int j = 0; j < si; ++j) skip |= (p.s[j].status[0] != 0x7f7f7f7f) || (p.s[j].status[1] != 0x7f7f7f7f);
-  const int k = b / s.chunks, ch = b % s.chunks;
   if (k == 0 && ch == 0 && threadIdx.x == 0) s.status[2] = skip ? 0 : 1;
   if (skip || !s.upd[k]) return;
   const float2 c = s.corr[k];
-  const int64_t base = int64_t(k) * s.block;
-  const int i = (ch * 256 + threadIdx.x) * 4;
-  if (i < s.block) adam_vec4(s.P + base, s.M + base, s.V + base, s.G + base, i, c.x, c.y, s.a);
+  if (in) {
+    adam_elem(pv.x, mv.x, vv.x, gv.x, c.x, c.y, s.a);
+    adam_elem(pv.y, mv.y, vv.y, gv.y, c.x, c.y, s.a);
+    adam_elem(pv.z, mv.z, vv.z, gv.z, c.x, c.y, s.a);
+    adam_elem(pv.w, mv.w, vv.w, gv.w, c.x, c.y, s.a);
+    st4(s.P + base + i, pv);
+    st4(s.M + base + i, mv);
+    st4(s.V + base + i, vv);
+  }
   if (ch == 0 && threadIdx.x == 0) s.step[k] += 1;
 #ifdef VM_TC_DEBUG
   if (threadIdx.x == 0) atomicAdd(&vm_tc_dbg[66], 1);
@@ -762,13 +781,13 @@ int plan_train(const VmStack* stacks, const VmBatch* batches, int n, TrainPlan& 
   pl.ws_bytes = off;
   return VM_OK;
 }
-// Partial reduce + Adam for stacks [first, last) on stream s.  Adam of stack
-// i reads the status words of stacks < i (trainer.py:368-388 raise order), so
-// a prefix of stacks can be finished before later stacks are done.
-int reduce_and_adam(const TrainPlan& pl, int n_stacks, int first, int last, cudaStream_t s) {
-  for (int i = first; i < last; ++i) {
+// Partial reduce of a tensor-core stack (its tiles' weight-gradient blocks;
+// FFMA stacks reduce in-kernel).  Runs on the tensor-core branch's stream so
+// it overlaps the FFMA kernel.
+int launch_reduce(const TrainPlan& pl, int i, cudaStream_t s) {
+  {
     const KStack& ks = pl.kp.s[i];
-    if (ks.P <= 1 || ks.K == 0 || !ks.tc) continue;  // FFMA stacks reduce in-kernel
+    if (ks.P <= 1 || ks.K == 0 || !ks.tc) return VM_OK;
     const int cf = red_chunk_floats(ks.P);
     const int grid = ks.K * ((ks.block + cf - 1) / cf);
     const int red_smem = ks.R * 3 * 4;
@@ -778,13 +797,16 @@ int reduce_and_adam(const TrainPlan& pl, int n_stacks, int first, int last, cuda
     VM_CUDA(cudaGetLastError());
     if (g_prof.on) g_prof.kernels += 1;
   }
-  const int b0 = pl.ap.s[first].item_base;
-  const int b1 = (last < n_stacks) ? pl.ap.s[last].item_base : pl.adam_grid;
-  if (b1 > b0) {
-    adam_train_kernel<<<b1 - b0, 256, 0, s>>>(pl.ap, b0);
-    VM_CUDA(cudaGetLastError());
-    if (g_prof.on) g_prof.kernels += 1;
-  }
+  return VM_OK;
+}
+
+// One Adam launch over every stack.  Adam of stack i reads the status words
+// of stacks < i (trainer.py:368-388 raise order).
+int launch_adam(const TrainPlan& pl, cudaStream_t s) {
+  if (pl.adam_grid <= 0) return VM_OK;
+  adam_train_kernel<<<pl.adam_grid, 256, 0, s>>>(pl.ap, 0);
+  VM_CUDA(cudaGetLastError());
+  if (g_prof.on) g_prof.kernels += 1;
   return VM_OK;
 }
 }  // namespace
@@ -947,21 +969,15 @@ extern "C" int vm_train_step(const VmStack* stacks, const VmBatch* batches, int 
     tck::tc_train_kernel<128, 4><<<ks.K * ks.P, tck::kTCThreads, smem_tc, ts>>>(pl.kp, i, img);
     VM_CUDA(cudaGetLastError());
     if (g_prof.on) g_prof.kernels += 1;
+    rc = launch_reduce(pl, i, ts);
+    if (rc) return rc;
   }
   if (kt1) VM_CUDA(cudaEventRecord(kt1, ts));
   if (!kf_done) {
     rc = launch_kf();
     if (rc) return rc;
   }
-  // stacks before the first tensor-core stack are finished on the main
-  // stream while the KT branch is still running
-  int tail_from = 0;
   if (forked) {
-    while (tail_from < n_stacks && !pl.kp.s[tail_from].tc) ++tail_from;
-    if (tail_from > 0) {
-      rc = reduce_and_adam(pl, n_stacks, 0, tail_from, s);
-      if (rc) return rc;
-    }
     VM_CUDA(cudaEventRecord(ev_join, side));
     VM_CUDA(cudaStreamWaitEvent(s, ev_join, 0));
   }
@@ -971,10 +987,8 @@ extern "C" int vm_train_step(const VmStack* stacks, const VmBatch* batches, int 
     g_prof.pair(r0, r1, 3);
     VM_CUDA(cudaEventRecord(r0, s));
   }
-  if (pl.adam_grid > 0) {
-    rc = reduce_and_adam(pl, n_stacks, tail_from, n_stacks, s);
-    if (rc) return rc;
-  }
+  rc = launch_adam(pl, s);
+  if (rc) return rc;
   if (r1) VM_CUDA(cudaEventRecord(r1, s));
   return VM_OK;
 }

@@ -125,9 +125,25 @@ __global__ void __launch_bounds__(256) tc_prep_kernel(const __grid_constant__ KS
 // |lo| <= 2^-11 |x|); the tensor core keeps lo's top 19 bits, so the split
 // error is <= 2^-22 |x|.  Two integer ALU ops + one FADD per element: the
 // ALU pipe (2 cycles per warp instruction per SMSP) bounds the staging.
+// Precision knobs (A/B builds): rounding lo to tf32 before the tensor core
+// reads it, and a 4th product lo.lo, change the weight-gradient error by < 1%
+// (measured, scripts/diag_kt_grad.py: ~3e-6 of max|g| either way) -- the
+// error is dominated by the tensor core's fp32 accumulation (truncating adds,
+// ~48 per 128-sample chain), not by the operand split -- so both stay off.
+#ifndef VM_KT_ROUND_LO
+#define VM_KT_ROUND_LO 0
+#endif
+#ifndef VM_KT_PRODUCTS
+#define VM_KT_PRODUCTS 3
+#endif
 __device__ __forceinline__ void split_fast(float x, float& hi, float& lo) {
   hi = __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
   lo = __fsub_rn(x, hi);
+#if VM_KT_ROUND_LO
+  // lo rounded to tf32 here (the tensor core would truncate it): x = hi + lo
+  // to ~2^-24 relative, so with the lo.lo product every tf32 product is exact
+  lo = __uint_as_float((__float_as_uint(lo) + 0x1000u) & 0xFFFFE000u);
+#endif
 }
 
 __device__ __forceinline__ uint32_t sw128_off(int row, int col) {
@@ -363,6 +379,7 @@ __global__ void __launch_bounds__(kTCThreads, 1)
             tc::mma_tf32(tm, al, bh, idesc, (ci.first && ks == 0) ? 0u : 1u);
             tc::mma_tf32(tm, ah, bl, idesc, 1u);
             tc::mma_tf32(tm, ah, bh, idesc, 1u);
+            if (VM_KT_PRODUCTS > 3) tc::mma_tf32(tm, al, bl, idesc, 1u);
           }
         } else if (ci.sw == 2) {
           const uint32_t idesc_mn = tc::idesc_tf32(128, ci.n, true, true);
@@ -374,6 +391,7 @@ __global__ void __launch_bounds__(kTCThreads, 1)
             tc::mma_tf32(tm, al, bh, idesc_mn, (ci.first && ks == 0) ? 0u : 1u);
             tc::mma_tf32(tm, ah, bl, idesc_mn, 1u);
             tc::mma_tf32(tm, ah, bh, idesc_mn, 1u);
+            if (VM_KT_PRODUCTS > 3) tc::mma_tf32(tm, al, bl, idesc_mn, 1u);
           }
         } else {
           const uint32_t a_lo = sa + ci.m_rows * 128, b_hi = sa + kHalfSlot, b_lo = b_hi + ci.n * 128;
@@ -384,6 +402,7 @@ __global__ void __launch_bounds__(kTCThreads, 1)
             tc::mma_tf32(tm, al, bh, idesc, (ci.first && ks == 0) ? 0u : 1u);
             tc::mma_tf32(tm, ah, bl, idesc, 1u);
             tc::mma_tf32(tm, ah, bh, idesc, 1u);
+            if (VM_KT_PRODUCTS > 3) tc::mma_tf32(tm, al, bl, idesc, 1u);
           }
         }
         tc::mma_commit(&empty[s]);

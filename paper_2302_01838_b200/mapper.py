@@ -11,6 +11,7 @@ kernel launches and one small D2H copy.
 
 from __future__ import annotations
 
+import os
 import time
 
 import numpy as np
@@ -30,7 +31,7 @@ class Mapper:
 
     def __init__(self, intrinsics: CameraIntrinsics, cfg: TrainConfig | None = None, device=DEVICE,
                  object_id_base: int = 0, init_index_base: int = 0, background_init_index: int = 0,
-                 use_graphs: bool = True):
+                 use_graphs: bool = True, fused_pe: bool | None = None):
         self.cfg = cfg if cfg is not None else TrainConfig()
         self.intrinsics = intrinsics
         self.device = torch.device(device)
@@ -57,6 +58,13 @@ class Mapper:
         self._buf_bg = None
         self._host_out = None
         self.use_graphs = use_graphs
+        # The sampler materialises the positional encoding in f64 -> f32
+        # exactly like models.py:286-308 (bit-identical MLP inputs); with
+        # fused_pe the MLP kernels encode f32 points on the fly instead
+        # (fewer bytes, f32 sincospif: tolerance-level inputs).
+        if fused_pe is None:
+            fused_pe = os.environ.get("VM_FUSED_PE", "0") == "1"
+        self.encode = not fused_pe
         self._g = None          # graph-replay state (see _graph_step)
         self._dev_tables = [(DeviceTable(self.device), DeviceTable(self.device)) for _ in range(2)]
         self._dirty = True
@@ -129,10 +137,11 @@ class Mapper:
                             self.device, dest=self._dev_tables[1]) if bg is not None else None
         K = len(objs)
         if K and (self._buf_obj is None or self._buf_obj.K != K):
-            self._buf_obj = SampleBuffers(K, c.rays_per_object, S, c.arch_object.input_dim, False, self.device)
+            self._buf_obj = SampleBuffers(K, c.rays_per_object, S, c.arch_object.input_dim, self.encode, self.device)
             self._g = None  # batch buffers reallocated: the step graphs must be recaptured
         if bg is not None and self._buf_bg is None:
-            self._buf_bg = SampleBuffers(1, c.rays_background, S, c.arch_background.input_dim, False, self.device)
+            self._buf_bg = SampleBuffers(1, c.rays_background, S, c.arch_background.input_dim, self.encode,
+                                         self.device)
             self._g = None
         # frozen bits live in persistent device buffers the graphs read
         if self.obj_params.count:
@@ -197,13 +206,14 @@ class Mapper:
         t_obj, t_bg = self._tables
         stacks = []
         if self.obj_params.count > 0:
-            p = sample_params(self.intrinsics, c.sampling, c.seed, step, c.rays_per_object, c.arch_object, False)
+            p = sample_params(self.intrinsics, c.sampling, c.seed, step, c.rays_per_object, c.arch_object,
+                              self.encode)
             run_sampler(self.arena, t_obj[0], t_obj[1], self.obj_params.count, p, self._buf_obj)
             stacks.append((self.obj_params, self.obj_state, self._buf_obj))
         bg = self.map.background
         if c.train_background and bg is not None:
             p = sample_params(self.intrinsics, c.sampling, c.seed, step, c.rays_background, c.arch_background,
-                              False)
+                              self.encode)
             run_sampler(self.arena, t_bg[0], t_bg[1], 1, p, self._buf_bg)
             stacks.append((self.bg_params, self.bg_state, self._buf_bg))
         if not stacks:
@@ -237,9 +247,9 @@ class Mapper:
         bg = self.map.background
         has_bg = c.train_background and bg is not None
         S = c.points_per_ray
-        bufs_o = [self._buf_obj, SampleBuffers(objs_n, c.rays_per_object, S, c.arch_object.input_dim, False, dev)
+        bufs_o = [self._buf_obj, SampleBuffers(objs_n, c.rays_per_object, S, c.arch_object.input_dim, self.encode, dev)
                   ] if objs_n else [None, None]
-        bufs_b = [self._buf_bg, SampleBuffers(1, c.rays_background, S, c.arch_background.input_dim, False, dev)
+        bufs_b = [self._buf_bg, SampleBuffers(1, c.rays_background, S, c.arch_background.input_dim, self.encode, dev)
                   ] if has_bg else [None, None]
         if objs_n:
             bufs_o[1].pe_scale.copy_(bufs_o[0].pe_scale)
@@ -248,16 +258,23 @@ class Mapper:
         step_dev = torch.zeros(1, dtype=torch.int64, device=dev)
         t_obj, t_bg = self._tables
 
-        def sample(p, offset):
+        def sample_obj(p, offset):
             if objs_n:
-                sp = sample_params(self.intrinsics, c.sampling, c.seed, 0, c.rays_per_object, c.arch_object, False)
+                sp = sample_params(self.intrinsics, c.sampling, c.seed, 0, c.rays_per_object, c.arch_object,
+                                   self.encode)
                 sp.step_dev, sp.step_offset = step_dev.data_ptr(), offset
                 run_sampler(self.arena, t_obj[0], t_obj[1], objs_n, sp, bufs_o[p])
+
+        def sample_bg(p, offset):
             if has_bg:
                 sp = sample_params(self.intrinsics, c.sampling, c.seed, 0, c.rays_background, c.arch_background,
-                                   False)
+                                   self.encode)
                 sp.step_dev, sp.step_offset = step_dev.data_ptr(), offset
                 run_sampler(self.arena, t_bg[0], t_bg[1], 1, sp, bufs_b[p])
+
+        def sample(p, offset):
+            sample_obj(p, offset)
+            sample_bg(p, offset)
 
         def stacks(p):
             out = []
@@ -276,6 +293,7 @@ class Mapper:
         host_l = torch.empty((n, 3), dtype=torch.float32, pin_memory=True)
         host_s = torch.empty(4 * len(stacks(0)), dtype=torch.int32, pin_memory=True)
         side = torch.cuda.Stream(dev)
+        side_bg = torch.cuda.Stream(dev)
         graphs = []
         for p in (0, 1):
             g = torch.cuda.CUDAGraph()
@@ -286,13 +304,20 @@ class Mapper:
                 # the garbage collector) must not invalidate this capture
                 with torch.cuda.graph(g, stream=main, capture_error_mode="relaxed"):
                     cur = torch.cuda.current_stream()
+                    # step t+1's objects and background are sampled on two
+                    # forked streams, concurrently with each other and with
+                    # step t's training
                     side.wait_stream(cur)
+                    side_bg.wait_stream(cur)
                     with torch.cuda.stream(side):
-                        sample(1 - p, 1)
+                        sample_obj(1 - p, 1)
+                    with torch.cuda.stream(side_bg):
+                        sample_bg(1 - p, 1)
                     losses, status = launch_train(stacks(p), c.loss_weights, self._ws, bump_version=False)
                     host_l.copy_(losses, non_blocking=True)
                     host_s.copy_(status, non_blocking=True)
                     cur.wait_stream(side)
+                    cur.wait_stream(side_bg)
                     _lib.check(_lib.load().vm_step_advance(step_dev.data_ptr(), 1, _lib.stream_ptr()),
                                "vm_step_advance")
             graphs.append(g)

@@ -6,8 +6,11 @@ name=$1; flags=$2
 root=$(cd "$(dirname "$0")/.." && pwd)
 out=$root/scripts/bin/$name
 mkdir -p $out/obj
-# objects that do not see the variant flags are reused from the main build
-for o in $root/paper_2302_01838_b200/_lib/obj/*.o; do case $(basename $o) in vm_kf32.o) ;; *) cp -p $o $out/obj/;; esac; done
-rm -f $out/obj/vm_kf32.o
+# objects listed in REBUILD (default: vm_kf32.o) are rebuilt with the flags,
+# the others are reused from the main build
+rebuild=${REBUILD:-vm_kf32.o}
+for o in $root/paper_2302_01838_b200/_lib/obj/*.o; do
+  case " $rebuild " in *" $(basename $o) "*) rm -f $out/obj/$(basename $o) ;; *) cp -p $o $out/obj/ ;; esac
+done
 make -s -C $root/paper_2302_01838_b200/csrc OUT=$out/libvmap_b200.so OBJDIR=$out/obj VMFLAGS="$flags" -j4 >/dev/null
 echo $out/libvmap_b200.so

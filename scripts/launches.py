@@ -7,7 +7,7 @@ path = sys.argv[1]
 lines = [l for l in open(path) if l.startswith('"')]
 rows = list(csv.reader(lines))
 h = rows[0]
-ours = ("sample_", "encode_kernel", "mlp_kernel", "reduce_partials", "adam_train", "adam_", "tc_train", "tc_prep")
+ours = ("sample_", "encode_kernel", "mlp_kernel", "kf32", "reduce_partials", "adam_train", "adam_", "tc_train", "tc_prep")
 agg = defaultdict(list)
 for r in rows[1:]:
     d = dict(zip(h, r))

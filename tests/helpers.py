@@ -55,6 +55,77 @@ def assert_params_rel_l2(params, ost: O.Stack, rel_l2=1e-4):
     assert rel.max() <= rel_l2, f"per-object relative L2 {rel.max():.3e} > {rel_l2}"
 
 
+def oracle_from_gpu(params, state, ost: O.Stack) -> O.Stack:
+    """Copy of the oracle stack `ost` loaded with the GPU's current model
+    state (weights, biases, Adam moments, step counters)."""
+    g = ost.copy()
+    k = params.count
+    W, B = host_layers(params)
+    mw, vw, mb, vb, st = host_state(state, k)
+    for l in range(len(W)):
+        g.W[l][:k], g.b[l][:k], g.mW[l][:k], g.vW[l][:k], g.mb[l][:k], g.vb[l][:k] = W[l], B[l], mw[l], vw[l], mb[l], vb[l]
+    g.step[:k] = st
+    return g
+
+
+def assert_step_close(params, state, o32: O.Stack, o64: O.Stack, rtol=1e-4, atol=1e-5, name="",
+                      max_off_frac=0.0, moment_rel_l2=None, param_rel_l2=None):
+    """Per-component one-step contract.  `o32` / `o64` are the reference's
+    f32 and f64 train steps applied to the GPU's previous state on the same
+    batch.  Every parameter and Adam moment must be within rtol/atol of the
+    f32 reference step, or -- on the reference's own knife-edges, where its
+    f32 and f64 steps disagree (a gradient summed to ~0 whose sign Adam's
+    early steps turn into +-lr, a ReLU / L1-sign flip) -- of the f64 step.
+
+    Relaxed form for the tensor-core (3xTF32) stacks, whose gradients carry
+    ~3e-6 x max|g| error (tensor-core fp32 accumulation): at most
+    `max_off_frac` of the parameters off both bands, every model within
+    `param_rel_l2` (relative L2) of the f32 or the f64 step, and the Adam
+    moments checked per model by relative L2 (`moment_rel_l2`) instead of
+    per component.  Returns (components off the f32 step, total)."""
+    W, B = host_layers(params)
+    k = params.count
+    mw, vw, mb, vb, st = host_state(state, k)
+    n_off32 = n_tot = n_bad = n_par = 0
+    flat = {"p": ([], [], []), "m": ([], [], [])}
+    for l in range(len(W)):
+        for nm, got, e32, e64 in (("W", W[l], o32.W[l], o64.W[l]), ("b", B[l], o32.b[l], o64.b[l]),
+                                  ("mW", mw[l], o32.mW[l], o64.mW[l]), ("mb", mb[l], o32.mb[l], o64.mb[l]),
+                                  ("vW", vw[l], o32.vW[l], o64.vW[l]), ("vb", vb[l], o32.vb[l], o64.vb[l])):
+            e32, e64 = e32[:k].astype(np.float64), e64[:k]
+            moment = nm[0] in "mv"
+            if moment and moment_rel_l2 is not None:
+                if nm[0] == "m":
+                    for lst, x in zip(flat["m"], (got, e32, e64)):
+                        lst.append(np.asarray(x, np.float64).reshape(k, -1))
+                continue
+            at = atol if nm[0] != "v" else atol * atol
+            c32 = np.abs(got - e32) <= at + rtol * np.abs(e32)
+            c64 = np.abs(got - e64) <= at + rtol * np.abs(e64)
+            bad = ~(c32 | c64)
+            n_off32 += int((~c32).sum())
+            n_tot += got.size
+            n_bad += int(bad.sum())
+            if not moment:
+                n_par += got.size
+                for lst, x in zip(flat["p"], (got, e32, e64)):
+                    lst.append(np.asarray(x, np.float64).reshape(k, -1))
+            if max_off_frac == 0.0:
+                assert not bad.any(), (f"{name} {nm}[{l}]: {int(bad.sum())} components off both the f32 and the "
+                                       f"f64 reference step; first {np.argwhere(bad)[0].tolist()}")
+    assert n_bad <= max_off_frac * max(n_par, 1), f"{name}: {n_bad} of {n_par} parameters off both bands"
+    if param_rel_l2 is not None:
+        g, r, r64 = (np.concatenate(x, 1) for x in flat["p"])
+        e = np.minimum(rel_l2(g, r), rel_l2(g, r64)).max()
+        assert e <= param_rel_l2, f"{name}: parameters {e:.2e} (relative L2) from the f32 / f64 reference step"
+    if moment_rel_l2 is not None:
+        g, r, r64 = (np.concatenate(x, 1) for x in flat["m"])
+        e = np.minimum(rel_l2(g, r), rel_l2(g, r64)).max()
+        assert e <= moment_rel_l2, f"{name}: first moments {e:.2e} (relative L2) from the f32 / f64 reference step"
+    np.testing.assert_array_equal(st, o32.step[:k])
+    return n_off32, n_tot
+
+
 def flat_params(params):
     W, B = host_layers(params)
     k = params.count

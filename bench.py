@@ -8,10 +8,19 @@ MLP fwd/render/loss/bwd kernel (KF) and batched Adam (KA).
   python bench.py [--gpus N --steps K --warmup W]      # this framework
   python bench.py --impl reference [...]               # reference CPU path
 
-N > 1 (torchrun, one rank per GPU): objects are sharded across ranks
-(weak scaling: 50 objects per rank, background on rank 0), losses gathered
-with NCCL all_gather every step.  Timing: CUDA events per step on the launch
-stream with an L2 flush (256 MiB write) between steps, max over ranks.
+N > 1: one process per GPU.  Without WORLD_SIZE in the environment,
+`--gpus N` re-launches itself under torch.distributed.run (127.0.0.1); under
+the driver's own torchrun WORLD_SIZE must equal N.  Workloads:
+  --workload 2 (default)  weak scaling: every rank maps one config-2 room
+                          (50 objects + its background, globally unique ids);
+  --workload 4            strong scaling: BASELINE config 4, one 1000-object
+                          map + background placed over the ranks by
+                          ObjectSharding.plan (cost-greedy), each object on
+                          exactly one rank with its global id and init key.
+Per step the per-object loss triples are all-gathered over NCCL (the only
+cross-rank traffic: objects are independent models).  Timing: CUDA events per
+step on the launch stream with an L2 flush (256 MiB write) between steps, max
+over ranks.
 """
 
 from __future__ import annotations
@@ -39,6 +48,28 @@ def flop_per_sample(hidden: int, input_dim: int = 33) -> int:
     mac_fwd = hidden * input_dim + 2 * hidden * hidden + 4 * hidden
     mac_dx = 2 * hidden * hidden + 4 * hidden
     return 2 * (2 * mac_fwd + mac_dx)
+
+
+def _free_port() -> int:
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def self_launch(args) -> None:
+    """--gpus N > 1 outside torchrun: re-exec under torch.distributed.run so the
+    driver's plain `python bench.py --gpus N` measures N ranks."""
+    env_world = os.environ.get("WORLD_SIZE")
+    if env_world is not None:
+        if args.gpus is not None and int(env_world) != args.gpus:
+            sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={env_world}")
+        return
+    if args.gpus is not None and args.gpus > 1:
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={_free_port()}", str(Path(__file__).resolve())]
+        cmd += sys.argv[1:]
+        os.execv(sys.executable, cmd)
 
 
 def dist_setup():
@@ -132,8 +163,7 @@ def run_reference(args, rank, world):
     pure Python/numpy and has no compiled build to run) on the box's host cores."""
     if rank != 0:
         return
-    from paper_2302_01838_b200.scenes import make_scene
-    scene = make_scene(OBJ_PER_RANK, n_kf=5, seed=0)
+    scene = workload_scene(args.workload, 0)
     import numpy as np  # noqa: F401
     from oracle import vobj_oracle as O
     from paper_2302_01838_b200 import TrainConfig
@@ -147,35 +177,54 @@ def run_reference(args, rank, world):
         O.map_update_step(ms)
         times.append(time.perf_counter() - t0)
     dt = sum(times) / len(times)
-    k = len(scene["objects"]) * world  # N rooms, as the GPU arm (timed on one host: N x the work)
-    dt = dt * world
+    k = len(scene["objects"])
+    if args.workload == "2":  # N rooms, as the GPU arm (timed on one host: N x the work)
+        k, dt = k * world, dt * world
     v = k / dt
     cores = blas_threads()
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
+        "scaling": "weak" if args.workload == "2" else "strong",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": _config(world),
+        "config": _config(world, args.workload),
         "samples_per_s": k * 120 * 10 / dt,
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": f"{args.steps} full map-update steps of config 2 (oracle/vobj_oracle.py "
+                         "sample": f"{args.steps} full map-update steps of config {args.workload} (oracle/vobj_oracle.py "
                                    f"map_update_step, numpy/OpenBLAS, {cores} threads)"},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }))
 
 
-def _config(world):
+def workload_scene(workload: str, rank: int) -> dict:
+    from paper_2302_01838_b200.scenes import config, make_scene
+    if workload == "2":   # this rank's own config-2 room
+        return make_scene(OBJ_PER_RANK, n_kf=5, seed=rank)
+    return config(workload)
+
+
+def _config(world, workload="2"):
+    if workload == "4":
+        return {"workload": "config 4: 1000 objects x 5 keyframes + background (config-2 style scene), one map "
+                            "placed over the ranks by ObjectSharding.plan (cost-greedy); full map update per step "
+                            "+ NCCL all-gather of the per-object losses",
+                "objects": 1000, "hidden_object": 32, "hidden_background": 128, "rays_per_object": 120,
+                "rays_background": 1200, "points_per_ray": 10, "frame": "1200x680",
+                "l2": "flushed (256 MiB write) between timed steps",
+                "parallelism": f"object-sharded x{world}" if world > 1 else "single GPU"}
     return {"workload": "config 2: Replica-sized synthetic scene, 50 objects x 5 keyframes + background; full "
                         "map update per step (ray/sample generation + fused MLP fwd/render/L1/bwd + Adam)",
             "objects_per_gpu": OBJ_PER_RANK, "objects": OBJ_PER_RANK * world, "hidden_object": 32,
             "hidden_background": 128, "rays_per_object": 120, "rays_background": 1200, "points_per_ray": 10,
             "frame": "1200x680", "l2": "flushed (256 MiB write) between timed steps",
-            "parallelism": f"object-sharded x{world}" if world > 1 else "single GPU"}
+            "parallelism": f"one config-2 room per GPU x{world}" if world > 1 else "single GPU"}
 
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--gpus", type=int, default=None)
+    ap.add_argument("--workload", default="2", choices=["2", "4"],
+                    help="BASELINE config: 2 = 50-object room per GPU (weak), 4 = 1000 objects sharded (strong)")
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
@@ -183,6 +232,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    self_launch(args)
 
     rank, world = dist_setup() if args.impl == "b200" else (int(os.environ.get("RANK", "0")),
                                                             int(os.environ.get("WORLD_SIZE", "1")))
@@ -198,16 +248,27 @@ def main():
 
     dev = torch.device("cuda", torch.cuda.current_device())
     lib = _lib.load()
-    # weak scaling: each rank maps one config-2 "room" (50 objects + its
-    # background); object ids / init keys are globally unique across ranks.
-    scene = make_scene(OBJ_PER_RANK, n_kf=5, seed=rank)
-    shard = ObjectSharding(world, [r for r in range(world) for _ in range(OBJ_PER_RANK)])
     cfg = TrainConfig()
-    mapper = Mapper(scene["intrinsics"], cfg, device=dev, object_id_base=rank * OBJ_PER_RANK,
-                    init_index_base=rank * OBJ_PER_RANK, background_init_index=rank)
-    populate(mapper, scene)
+    scene = workload_scene(args.workload, rank)
+    if args.workload == "2":
+        # weak scaling: each rank maps one config-2 "room" (50 objects + its
+        # background); object ids / init keys are globally unique across ranks.
+        shard = ObjectSharding(world, [r for r in range(world) for _ in range(OBJ_PER_RANK)], rooms=True)
+        mapper = Mapper(scene["intrinsics"], cfg, device=dev, object_id_base=rank * OBJ_PER_RANK,
+                        init_index_base=rank * OBJ_PER_RANK, background_init_index=rank)
+        populate(mapper, scene)
+        k_total = OBJ_PER_RANK * world
+    else:
+        # strong scaling: one map, each object on exactly one rank (global id
+        # and init key kept), the background on the rank the cost plan picks
+        shard = ObjectSharding.plan(scene, world, cfg.rays_per_object, cfg.rays_background, cfg.points_per_ray,
+                                    cfg.arch_object.hidden, cfg.arch_background.hidden)
+        mapper = Mapper(scene["intrinsics"], cfg, device=dev)
+        populate(mapper, scene, objects=set(shard.objects_of(rank)),
+                 with_background=(rank == shard.background_rank))
+        k_total = len(scene["objects"])
     k_local = mapper.obj_params.count
-    k_total = OBJ_PER_RANK * world
+    has_bg = mapper.map.background is not None
 
     # FP32 FFMA peak (roofline denominator; MEASURED_PEAKS.json has no FP32 entry)
     tf = C.c_float()
@@ -232,7 +293,7 @@ def main():
             ev[i][0].record(stream)
             mapper.enqueue_graph_step(mapper.global_step)
             if world > 1:
-                shard.gather_losses_device(mapper._ws.losses[:k_local + 1])
+                shard.gather_losses_device(mapper._ws.losses[:k_local + has_bg])
             ev[i][1].record(stream)
             mapper.global_step += 1
         torch.cuda.synchronize()
@@ -302,7 +363,8 @@ def main():
     # FFMA) and KT (background, tcgen05 3xTF32 + its weight-image prep) run
     # concurrently on two streams; the MLP phase is fork .. join.
     flop_obj = k_local * cfg.rays_per_object * cfg.points_per_ray * flop_per_sample(32)
-    flop_bg = (cfg.rays_background * cfg.points_per_ray * flop_per_sample(128)) if cfg.train_background else 0
+    flop_bg = (cfg.rays_background * cfg.points_per_ray * flop_per_sample(128)) if (cfg.train_background
+                                                                                    and has_bg) else 0
     flop_launch = flop_obj + flop_bg
     kernel_ms = mlp_ms.value / max(n_launch.value, 1)
     traffic = traffic_tc = None
@@ -320,7 +382,7 @@ def main():
     if per_tag.get(1):
         a = flop_obj / (per_tag[1] * 1e-3) / 1e12
         kernels.append({"bound": "fp32", "achieved": a, "peak": ffma_peak, "unit": "TFLOP/s", "frac": a / ffma_peak,
-                        "traffic": traffic, "kernel": "mlp_kernel (KF, FFMA, hidden-32 objects)",
+                        "traffic": traffic, "kernel": "kf32_train_kernel (KF, FFMA, hidden-32 objects)",
                         "kernel_ms": per_tag[1], "flop_per_launch": flop_obj,
                         "peak_source": "FP32 FFMA throughput measured in this run by vm_ffma_peak "
                                        "(MEASURED_PEAKS.json has no FP32 entry)"})
@@ -345,14 +407,15 @@ def main():
         v, n, dt = cpu_sample(scene, args.cpu_seconds)
         cores = blas_threads()
         cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
-               "sample": f"{n} full map-update steps of config 2 ({dt*1e3:.0f} ms/step) through "
+               "sample": f"{n} full map-update steps of config {args.workload} ({dt*1e3:.0f} ms/step) through "
                          f"oracle/vobj_oracle.py map_update_step (numpy/OpenBLAS, {cores} threads)"}
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": _config(world),
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "weak" if args.workload == "2" else "strong",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": _config(world, args.workload),
             "samples_per_s": value * cfg.rays_per_object * cfg.points_per_ray,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "gpu_launches": kernels_per_step * args.steps,

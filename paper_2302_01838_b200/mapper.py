@@ -79,12 +79,21 @@ class Mapper:
         scale = self.cfg.pe_scale_background if pe_scale is None else pe_scale
         return self.map.add_background(aabb, scale, idx)
 
-    def add_object(self, semantic_class: int, aabb, pe_scale: float | None = None):
-        """append_model + ObjectMap.add_object + model_to_object (trainer.py:254-256)."""
+    def add_object(self, semantic_class: int, aabb, pe_scale: float | None = None, object_id: int | None = None,
+                   init_index: int | None = None):
+        """append_model + ObjectMap.add_object + model_to_object (trainer.py:254-256).
+
+        `object_id` / `init_index` place a shard of a global map: the object
+        keeps its global id (sampling streams are keyed by it, objects.py:335)
+        and its global append index as the init key (models.py:264-267,
+        SURVEY 8e init-key caveat), so every rank reproduces the single-stack
+        run for the objects it owns."""
+        if init_index is None:
+            init_index = self._init_base + self.obj_params.count
         idx = append_model(self.obj_params, self.obj_state, self.cfg.seed, PURPOSE_INIT_OBJECT,
-                           init_index=self._init_base + self.obj_params.count)
+                           init_index=init_index)
         scale = self.cfg.pe_scale_object if pe_scale is None else pe_scale
-        inst = self.map.add_object(semantic_class, aabb, scale, idx)
+        inst = self.map.add_object(semantic_class, aabb, scale, idx, object_id=object_id)
         self.model_to_object.append(inst.object_id)
         return inst
 

@@ -87,9 +87,17 @@ class ObjectMap:
         self.instances[0] = inst
         return inst
 
-    def add_object(self, semantic_class: int, aabb: AABB, pe_scale: float, model_index: int) -> ObjectInstance:
-        oid = self._next_id
-        self._next_id += 1
+    def add_object(self, semantic_class: int, aabb: AABB, pe_scale: float, model_index: int,
+                   object_id: int | None = None) -> ObjectInstance:
+        """objects.py:140-147.  `object_id` pins the id (object-sharded ranks
+        register their share of a global map under the global ids)."""
+        if object_id is None:
+            oid = self._next_id
+        else:
+            oid = int(object_id)
+            if oid <= 0 or oid in self.instances:
+                raise ValueError(f"object id {oid} is reserved or already registered")
+        self._next_id = max(self._next_id, oid + 1)
         inst = ObjectInstance(oid, semantic_class, aabb, pe_scale, model_index)
         self.instances[oid] = inst
         return inst

@@ -62,8 +62,9 @@ def config(name: str) -> dict:
 def populate(mapper, scene: dict, objects=None, with_background: bool = True) -> None:
     """Register the scene's background/objects/keyframes in a Mapper.
 
-    ``objects`` optionally restricts to a subset of object indices (used by
-    the multi-GPU sharding).
+    ``objects`` optionally restricts to a subset of object indices (a rank's
+    share under multi-GPU object sharding): object i then keeps its global id
+    i + 1 and global init index i, exactly as in the unsharded map.
     """
     if scene["background"] is not None and with_background:
         bg = mapper.add_background(scene["background"]["aabb"])
@@ -73,7 +74,10 @@ def populate(mapper, scene: dict, objects=None, with_background: bool = True) ->
     for i, ob in enumerate(scene["objects"]):
         if objects is not None and i not in objects:
             continue
-        inst = mapper.add_object(1, ob["aabb"])
+        if objects is None:
+            inst = mapper.add_object(1, ob["aabb"])
+        else:
+            inst = mapper.add_object(1, ob["aabb"], object_id=i + 1, init_index=i)
         for kf in ob["keyframes"]:
             mapper.add_keyframe(inst, kf["frame_id"], kf["pose"], kf["bbox"], kf["mask"], scene["rgb"],
                                 scene["depth"])

@@ -45,6 +45,7 @@ class ObjectSharding:
     world: int
     owner: list            # owner rank per global object index
     background_rank: int = 0
+    rooms: bool = False    # one independent map per rank (weak scaling) instead of one sharded map
     _gather_buf: torch.Tensor | None = field(default=None, repr=False)
 
     @staticmethod
@@ -80,25 +81,27 @@ class ObjectSharding:
 
     def gather_losses(self, report) -> dict | None:
         """Host-level gather of StepReport.losses (object id -> triple) to every
-        rank; returns the merged dict."""
+        rank; returns the merged dict.  With `rooms` (independent maps per
+        rank, each with its own background id 0) the keys are (rank, id)."""
         if self.world == 1:
             return dict(report.losses)
         import torch.distributed as dist
         ids = sorted(report.losses)
         kmax = max(sum(1 for r in self.owner if r == q) for q in range(self.world)) + 1
-        import torch.distributed as dist
         dev = (torch.device("cuda", torch.cuda.current_device()) if dist.get_backend() == "nccl"
                else torch.device("cpu"))
-        send = torch.full((kmax, 4), -1.0, dtype=torch.float64, device=dev)
+        rank = dist.get_rank()
+        rows = np.full((kmax, 5), -1.0, dtype=np.float64)
         for j, oid in enumerate(ids):
-            send[j, 0] = oid
-            send[j, 1:] = torch.tensor(report.losses[oid], dtype=torch.float64)
-        out = torch.empty((self.world * kmax, 4), dtype=torch.float64, device=dev)
+            rows[j] = (rank, oid, *report.losses[oid])
+        send = torch.from_numpy(rows).to(dev)
+        out = torch.empty((self.world * kmax, 5), dtype=torch.float64, device=dev)
         _all_gather(out.view(self.world, -1), send.view(-1))
         merged = {}
         for row in out.cpu().numpy():
             if row[0] >= 0:
-                merged[int(row[0])] = (float(row[1]), float(row[2]), float(row[3]))
+                key = (int(row[0]), int(row[1])) if self.rooms else int(row[1])
+                merged[key] = (float(row[2]), float(row[3]), float(row[4]))
         return merged
 
 

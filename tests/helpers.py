@@ -174,9 +174,11 @@ class _NS:
         self.__dict__.update(kw)
 
 
-def oracle_mapstate(scene, cfg, obj_hidden=32, bg_hidden=128):
+def oracle_mapstate(scene, cfg, obj_hidden=32, bg_hidden=128, objects=None, with_background=True):
     """Oracle MapState populated from a scenes.make_scene dict (same init keys
-    as Mapper: append order, PURPOSE_INIT_OBJECT / PURPOSE_INIT_BACKGROUND)."""
+    as Mapper: append order, PURPOSE_INIT_OBJECT / PURPOSE_INIT_BACKGROUND).
+    `objects` restricts it to a shard: object i keeps id i + 1 and init key i
+    (scenes.populate's sharded form)."""
     intr = scene["intrinsics"]
 
     def kfs(spec):
@@ -190,15 +192,23 @@ def oracle_mapstate(scene, cfg, obj_hidden=32, bg_hidden=128):
 
     ao = O.Arch(cfg.arch_object.n_layers, cfg.arch_object.hidden, cfg.arch_object.n_freq)
     ab = O.Arch(cfg.arch_background.n_layers, cfg.arch_background.hidden, cfg.arch_background.n_freq)
-    objs = []
+    objs, keys = [], []
     for i, spec in enumerate(scene["objects"]):
+        if objects is not None and i not in objects:
+            continue
         objs.append(_NS(object_id=i + 1, keyframes=kfs(spec), aabb=spec["aabb"], pe_scale=cfg.pe_scale_object,
-                        active=True, model_index=i))
+                        active=True, model_index=len(objs)))
+        keys.append(i)
     bg = None
-    if scene["background"] is not None:
+    if scene["background"] is not None and with_background:
         bg = _NS(object_id=0, keyframes=kfs(scene["background"]), aabb=scene["background"]["aabb"],
                  pe_scale=cfg.pe_scale_background, active=True, model_index=0)
     ost = O.new_stack(ao, len(objs), cfg.seed, O.INIT_OBJECT)
+    for k, i in enumerate(keys):
+        if i != k:  # global init key of a sharded object
+            ws, bs = O.init_model_arrays(ao, cfg.seed, i, O.INIT_OBJECT)
+            for l in range(len(ws)):
+                ost.W[l][k], ost.b[l][k] = ws[l], bs[l]
     bst = O.new_stack(ab, 1 if bg else 0, cfg.seed, O.INIT_BACKGROUND)
     samp = O.Sampling(cfg.sampling.t_near, cfg.sampling.t_far, cfg.sampling.n_stratified,
                       cfg.sampling.n_surface, cfg.sampling.surface_std)

@@ -75,3 +75,26 @@ def test_unknown_mode_rejected(cuda):
     m = Mapper(scene["intrinsics"], TrainConfig())
     with pytest.raises(ValueError, match="mode"):
         m.train_step(mode="turbo")
+
+
+def test_sharded_shard_matches_oracle_shard(cuda):
+    """One rank's share of a cost-planned 2-rank map (global ids, global init
+    keys, background on the plan's rank) on this GPU reproduces the oracle's
+    shard, which the gloo test shows equals the unsharded map update."""
+    from paper_2302_01838_b200.sharding import ObjectSharding
+    scene = make_scene(7, n_kf=2, width=160, height=120, focal=100.0, crop=(20, 60), n_kf_bg=1, seed=5)
+    cfg = TrainConfig(rays_per_object=24, rays_background=40)
+    shard = ObjectSharding.plan(scene, 2, cfg.rays_per_object, cfg.rays_background, cfg.points_per_ray)
+    for rank in (0, 1):
+        mine = set(shard.objects_of(rank))
+        m = Mapper(scene["intrinsics"], cfg)
+        populate(m, scene, objects=mine, with_background=(rank == shard.background_rank))
+        ms = oracle_mapstate(scene, cfg, objects=mine, with_background=(rank == shard.background_rank))
+        for s in range(3):
+            rep = m.train_step()
+            exp = O.map_update_step(ms)
+            assert sorted(rep.losses) == sorted(exp) == sorted([i + 1 for i in mine] +
+                                                               ([0] if rank == shard.background_rank else []))
+            for oid, trip in exp.items():
+                np.testing.assert_allclose(np.array(rep.losses[oid]), np.array(trip), rtol=1e-4, atol=1e-5)
+        assert_params_close(m.obj_params, ms.obj)

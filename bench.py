@@ -132,14 +132,13 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def cpu_sample(scene, seconds: float, min_steps: int = 3):
-    """Time the oracle port (numpy restatement of the reference) on config 2."""
+def cpu_sample(scene, seconds: float, cfg, min_steps: int = 3):
+    """Time the oracle port (numpy restatement of the reference) on the workload."""
     import numpy as np
     from oracle import vobj_oracle as O
-    from paper_2302_01838_b200 import TrainConfig
     sys.path.insert(0, str(ROOT / "tests"))
     from tests.helpers import oracle_mapstate
-    ms = oracle_mapstate(scene, TrainConfig())
+    ms = oracle_mapstate(scene, cfg)
     O.map_update_step(ms)  # warm-up (BLAS threads, page faults)
     n, t0 = 0, time.perf_counter()
     while n < min_steps or time.perf_counter() - t0 < seconds:
@@ -166,9 +165,8 @@ def run_reference(args, rank, world):
     scene = workload_scene(args.workload, 0)
     import numpy as np  # noqa: F401
     from oracle import vobj_oracle as O
-    from paper_2302_01838_b200 import TrainConfig
     from tests.helpers import oracle_mapstate
-    ms = oracle_mapstate(scene, TrainConfig())
+    ms = oracle_mapstate(scene, workload_cfg(args.workload))
     for _ in range(max(args.warmup, 1)):
         O.map_update_step(ms)
     times = []
@@ -188,12 +186,17 @@ def run_reference(args, rank, world):
         "scaling": "weak" if args.workload == "2" else "strong",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": _config(world, args.workload),
-        "samples_per_s": k * 120 * 10 / dt,
+        "samples_per_s": k * 10 * float(np.mean([ob.get("n_rays", 120) for ob in scene["objects"]])) / dt,
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
                          "sample": f"{args.steps} full map-update steps of config {args.workload} (oracle/vobj_oracle.py "
                                    f"map_update_step, numpy/OpenBLAS, {cores} threads)"},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }))
+
+
+def workload_cfg(workload: str):
+    from paper_2302_01838_b200 import TrainConfig
+    return TrainConfig(rays_per_object=480) if workload == "3" else TrainConfig()
 
 
 def workload_scene(workload: str, rank: int) -> dict:
@@ -204,6 +207,13 @@ def workload_scene(workload: str, rank: int) -> dict:
 
 
 def _config(world, workload="2"):
+    if workload == "3":
+        return {"workload": "config 3: 200 objects x 10 keyframes + background, per-object rays log-uniform in "
+                            "[30, 480] (batch width 480, ray_ok=False padding); full map update per step",
+                "objects": 200, "hidden_object": 32, "hidden_background": 128, "rays_per_object": "30..480",
+                "rays_background": 1200, "points_per_ray": 10, "frame": "1200x680",
+                "l2": "flushed (256 MiB write) between timed steps",
+                "parallelism": f"object-sharded x{world}" if world > 1 else "single GPU"}
     if workload == "4":
         return {"workload": "config 4: 1000 objects x 5 keyframes + background (config-2 style scene), one map "
                             "placed over the ranks by ObjectSharding.plan (cost-greedy); full map update per step "
@@ -223,7 +233,7 @@ def _config(world, workload="2"):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=None)
-    ap.add_argument("--workload", default="2", choices=["2", "4"],
+    ap.add_argument("--workload", default="2", choices=["2", "3", "4"],
                     help="BASELINE config: 2 = 50-object room per GPU (weak), 4 = 1000 objects sharded (strong)")
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
@@ -248,7 +258,7 @@ def main():
 
     dev = torch.device("cuda", torch.cuda.current_device())
     lib = _lib.load()
-    cfg = TrainConfig()
+    cfg = workload_cfg(args.workload)
     scene = workload_scene(args.workload, rank)
     if args.workload == "2":
         # weak scaling: each rank maps one config-2 "room" (50 objects + its
@@ -362,7 +372,8 @@ def main():
     # launch (same step, eager replay with L2 flushed).  KF (objects, FP32
     # FFMA) and KT (background, tcgen05 3xTF32 + its weight-image prep) run
     # concurrently on two streams; the MLP phase is fork .. join.
-    flop_obj = k_local * cfg.rays_per_object * cfg.points_per_ray * flop_per_sample(32)
+    rays_obj = sum(int(mapper.instance_for_model(i).n_rays or cfg.rays_per_object) for i in range(k_local))
+    flop_obj = rays_obj * cfg.points_per_ray * flop_per_sample(32)
     flop_bg = (cfg.rays_background * cfg.points_per_ray * flop_per_sample(128)) if (cfg.train_background
                                                                                     and has_bg) else 0
     flop_launch = flop_obj + flop_bg
@@ -404,7 +415,7 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, n, dt = cpu_sample(scene, args.cpu_seconds)
+        v, n, dt = cpu_sample(scene, args.cpu_seconds, cfg)
         cores = blas_threads()
         cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
                "sample": f"{n} full map-update steps of config {args.workload} ({dt*1e3:.0f} ms/step) through "
@@ -416,7 +427,7 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "weak" if args.workload == "2" else "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": _config(world, args.workload),
-            "samples_per_s": value * cfg.rays_per_object * cfg.points_per_ray,
+            "samples_per_s": (rays_obj / max(k_local, 1)) * value * cfg.points_per_ray,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "gpu_launches": kernels_per_step * args.steps,
             "roofline": dominant,

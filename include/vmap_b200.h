@@ -90,7 +90,16 @@ typedef struct VmStack {
 /* RaySampleBatch (trainer.py:162-173), stacked on a leading model axis.
    Either `encoded` [K,R,S,D] (reference layout) or `points` [K,R,S,3]
    (box-normalised sample points; positional encoding fused in-kernel with
-   `pe_scale` [K]) must be given. */
+   `pe_scale` [K]) must be given.
+
+   Mixed per-object ray counts (BASELINE config 3): `model_rays`
+   [K] (device, optional) gives the rays model k drew (<= n_rays); its rows
+   r >= model_rays[k] are zero padding with ray_ok = 0 -- exactly the
+   reference's _zero_batch rows (trainer.py:190-200), which contribute
+   nothing to losses (render.py:301-308) or gradients (render.py:324-333).
+   The FFMA object kernel skips them; `work_items` [2*n_work_items] (device,
+   (model, chunk) pairs from vm_work_items) lets its grid cover only the live
+   chunks (NULL: a K x max-chunks grid whose dead chunks exit at once). */
 typedef struct VmBatch {
   int32_t n_models, n_rays, n_points, input_dim;
   const float* encoded;
@@ -102,6 +111,9 @@ typedef struct VmBatch {
   const uint8_t* target_mask;  /* [K,R] */
   const uint8_t* valid_depth;  /* [K,R] */
   const uint8_t* ray_ok;       /* [K,R] */
+  const int32_t* model_rays;   /* [K] live rays per model, or NULL (all n_rays) */
+  const int32_t* work_items;   /* [2*n_work_items] (model, chunk), or NULL */
+  int32_t n_work_items, reserved;
 } VmBatch;
 
 /* LossWeights (render.py:61-64). */
@@ -125,6 +137,13 @@ int vm_model_layout(const VmArch* arch, VmLayout* out);
    skipped (no Adam) when an earlier stack reported a non-finite gradient or
    loss, matching the reference's raise-before-next-stack order. ----------- */
 size_t vm_train_workspace_bytes(const VmStack* stacks, const VmBatch* batches, int n_stacks);
+/* Work items of the FFMA object kernel for per-model ray counts
+   `model_rays` (host [n_models]): (model, chunk) pairs written to `items`
+   (host, 2*capacity int32; may be NULL to query), count in *n_items.  The
+   chunking depends only on each model's own ray count (vectorised ==
+   sequential bits). */
+int vm_work_items(const int32_t* model_rays, int32_t n_models, int32_t n_points, int32_t* items,
+                  int32_t capacity, int32_t* n_items);
 int vm_train_step(const VmStack* stacks, const VmBatch* batches, int n_stacks,
                   VmLossWeights weights, float* losses /* [sum K][3] */,
                   int32_t* status /* device [4*n_stacks] */,
@@ -176,7 +195,8 @@ typedef struct VmSampleObject {
   int64_t object_id;           /* RNG key part (objects.py:335, trainer.py:304) */
   int32_t kf_begin, n_kf;      /* keyframes [kf_begin, kf_begin+n_kf) */
   int32_t active;              /* 0 -> zero batch (trainer.py:272-273, :336-338) */
-  int32_t reserved;
+  int32_t n_rays;              /* rays this object draws (<= params n_rays; 0: params n_rays);
+                                  rows beyond are zero padding (config 3) */
   double box_min[3], box_max[3];   /* padded AABB (geometry.py:40-42) */
   double center[3], half[3];       /* of the padded AABB */
   double pe_scale;

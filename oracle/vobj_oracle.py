@@ -483,6 +483,24 @@ def assemble_batch(inst, intr, arch: Arch, n_rays: int, step: int, seed: int,
     return out
 
 
+def pad_batch(b: dict, rays: int, points: int, input_dim: int) -> dict:
+    """Config 3: an object that drew fewer rays than the batch
+    width is padded with the reference's zero-batch rows (trainer.py:190-200,
+    ray_ok = False), which render.py:301-333 excludes from every loss and
+    gradient term."""
+    n = b["t"].shape[0]
+    if n == rays:
+        return b
+    z = zero_batch(rays - n, points, input_dim)
+    return {key: np.concatenate([b[key], z[key]]) for key in b}
+
+
+def object_rays(inst, default: int) -> int:
+    """Rays this instance draws: its own count (config 3) or the batch width."""
+    n = getattr(inst, "n_rays", None)
+    return int(n) if n else default
+
+
 def stack_batches(batches: list) -> dict:
     """trainer.py:320-330."""
     return {key: np.stack([b[key] for b in batches]) for key in batches[0]}
@@ -521,8 +539,10 @@ def map_update_step(ms: MapState) -> dict:
             if ms.obj.frozen[k]:
                 bs.append(zero_batch(ms.rays_object, pts, ms.obj.arch.input_dim))
             else:
-                bs.append(assemble_batch(ms.objects[k], ms.intr, ms.obj.arch, ms.rays_object, step,
-                                         ms.seed, ms.sampling, ms.bound_pad))
+                nr = object_rays(ms.objects[k], ms.rays_object)
+                b = assemble_batch(ms.objects[k], ms.intr, ms.obj.arch, nr, step, ms.seed, ms.sampling,
+                                   ms.bound_pad)
+                bs.append(pad_batch(b, ms.rays_object, pts, ms.obj.arch.input_dim))
         ld, lc, lo = train_on_batch(ms.obj, stack_batches(bs), ms.w_colour, ms.w_occ)
         for k in range(ms.obj.count):
             vals = (ld[k], lc[k], lo[k])

@@ -47,7 +47,9 @@ class VmBatch(C.Structure):
                 ("input_dim", C.c_int32),
                 ("encoded", C.c_void_p), ("points", C.c_void_p), ("pe_scale", C.c_void_p),
                 ("t", C.c_void_p), ("target_depth", C.c_void_p), ("target_colour", C.c_void_p),
-                ("target_mask", C.c_void_p), ("valid_depth", C.c_void_p), ("ray_ok", C.c_void_p)]
+                ("target_mask", C.c_void_p), ("valid_depth", C.c_void_p), ("ray_ok", C.c_void_p),
+                ("model_rays", C.c_void_p), ("work_items", C.c_void_p), ("n_work_items", C.c_int32),
+                ("reserved", C.c_int32)]
 
 
 class VmLossWeights(C.Structure):
@@ -61,7 +63,7 @@ class VmKeyframe(C.Structure):
 
 class VmSampleObject(C.Structure):
     _fields_ = [("object_id", C.c_int64), ("kf_begin", C.c_int32), ("n_kf", C.c_int32),
-                ("active", C.c_int32), ("reserved", C.c_int32),
+                ("active", C.c_int32), ("n_rays", C.c_int32),
                 ("box_min", C.c_double * 3), ("box_max", C.c_double * 3),
                 ("center", C.c_double * 3), ("half", C.c_double * 3), ("pe_scale", C.c_double)]
 
@@ -84,6 +86,7 @@ class VmSampleAux(C.Structure):
 _SIGNATURES = {
     "vm_model_layout": (C.c_int, [C.POINTER(VmArch), C.POINTER(VmLayout)]),
     "vm_train_workspace_bytes": (C.c_size_t, [C.POINTER(VmStack), C.POINTER(VmBatch), C.c_int]),
+    "vm_work_items": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_int32, C.POINTER(C.c_int32)]),
     "vm_train_step": (C.c_int, [C.POINTER(VmStack), C.POINTER(VmBatch), C.c_int, VmLossWeights,
                                 C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]),
     "vm_forward": (C.c_int, [C.POINTER(VmStack), C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,

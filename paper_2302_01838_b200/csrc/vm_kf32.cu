@@ -239,8 +239,15 @@ __global__ void __launch_bounds__(NTHR, 2) kf32_train_kernel(const __grid_consta
   item -= st.item_base;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int team = warp / T, wt = warp % T, o0 = wt * OW;
-  const int k = item / st.P, split = item % st.P;
+  const int k = st.items ? st.items[2 * item] : item / st.P;
+  const int split = st.items ? st.items[2 * item + 1] : item % st.P;
   const int S = SFIX > 0 ? SFIX : st.S, G = kSB / S;
+  // this model's live rays (config 3: padding rows beyond are skipped) and
+  // its chunking, a function of its own ray count only
+  const int Rk = st.model_rays ? min(st.model_rays[k], st.R) : st.R;
+  const int nblk = (Rk + G - 1) / G;
+  const int Pk = max(1, (nblk + st.chunk - 1) / st.chunk);
+  if (split >= Pk) return;  // dead chunk of a short model (grid without a work-item table)
 
   // ---- stage the model's weights (rows of stride WS) and biases
   float* sW = smem;
@@ -271,8 +278,7 @@ __global__ void __launch_bounds__(NTHR, 2) kf32_train_kernel(const __grid_consta
   float* tS = base + kRows * kLD;
   __syncthreads();
 
-  const int nblk = (st.R + G - 1) / G;
-  const int bps = (nblk + st.P - 1) / st.P;
+  const int bps = (nblk + Pk - 1) / Pk;
   const int blk0 = split * bps, blk1 = min(nblk, blk0 + bps);
 
   Grads acc;
@@ -306,7 +312,7 @@ __global__ void __launch_bounds__(NTHR, 2) kf32_train_kernel(const __grid_consta
 
   for (int blk = blk0 + team; blk < blk1; blk += NT) {
     const int r_begin = blk * G;
-    const int nr = min(G, st.R - r_begin);
+    const int nr = min(G, Rk - r_begin);
     const int ns = nr * S;
     const int64_t gs0 = (int64_t(k) * st.R + r_begin) * S;
 
@@ -553,7 +559,7 @@ __global__ void __launch_bounds__(NTHR, 2) kf32_train_kernel(const __grid_consta
   }
   __syncthreads();
   const int k_block = st.block;
-  float* gdst = (st.P == 1) ? st.grads + int64_t(k) * k_block : st.partials + (int64_t(k) * st.P + split) * k_block;
+  float* gdst = (Pk == 1) ? st.grads + int64_t(k) * k_block : st.partials + (int64_t(k) * st.P + split) * k_block;
   {
     const float* r0 = smem + kWFloats;
     for (int i = tid; i < k_block / 4; i += NTHR) {
@@ -569,11 +575,11 @@ __global__ void __launch_bounds__(NTHR, 2) kf32_train_kernel(const __grid_consta
 
   // ---------------- per-model finalisation (last chunk to finish) ---------
   bool finite = true;
-  if (st.P > 1) {
+  if (Pk > 1) {
     __shared__ int s_last;
     __threadfence();
     __syncthreads();
-    if (tid == 0) s_last = atomicAdd(&st.counters[k], 1) == st.P - 1;
+    if (tid == 0) s_last = atomicAdd(&st.counters[k], 1) == Pk - 1;
     __syncthreads();
     if (!s_last) return;
     __threadfence();
@@ -581,7 +587,7 @@ __global__ void __launch_bounds__(NTHR, 2) kf32_train_kernel(const __grid_consta
     float* gw = st.grads + int64_t(k) * k_block;
     for (int i = tid; i < k_block / 4; i += NTHR) {
       float4 v = __ldcg(reinterpret_cast<const float4*>(pb + 4 * i));
-      for (int u = 1; u < st.P; ++u) {
+      for (int u = 1; u < Pk; ++u) {
         const float4 w = __ldcg(reinterpret_cast<const float4*>(pb + int64_t(u) * k_block + 4 * i));
         v.x += w.x; v.y += w.y; v.z += w.z; v.w += w.w;
       }

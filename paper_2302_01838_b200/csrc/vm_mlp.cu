@@ -745,6 +745,11 @@ int plan_train(const VmStack* stacks, const VmBatch* batches, int n, TrainPlan& 
     ks.tmask = b.target_mask;
     ks.valid = b.valid_depth;
     ks.ok = b.ray_ok;
+    ks.chunk = chunk_blocks();
+    ks.model_rays = b.model_rays;
+    ks.items = b.model_rays ? b.work_items : nullptr;
+    ks.n_items = ks.items ? b.n_work_items : 0;
+    VM_REQUIRE(!ks.items || ks.n_items >= 0, "vm_train_step: bad work-item count");
     ks.tc = tc_enabled() && ks.H == 128 && ks.L == 4 && ks.D <= tck::kK0 && ks.S <= 32 ? 1 : 0;
   }
   choose_splits(pl.kp.s, n, P);
@@ -753,7 +758,7 @@ int plan_train(const VmStack* stacks, const VmBatch* batches, int n, TrainPlan& 
     ks.P = P[i];
     ks.item_base = item_base;
     ks.model_base = model_base;
-    item_base += ks.K * ks.P;
+    item_base += ks.items ? ks.n_items : ks.K * ks.P;
     model_base += ks.K;
     const size_t K = size_t(ks.K);
     pl.off_grads[i] = off; off = align_up(off + K * ks.block * 4, 256);
@@ -811,6 +816,29 @@ int launch_adam(const TrainPlan& pl, cudaStream_t s) {
 }
 }  // namespace
 
+extern "C" int vm_work_items(const int32_t* model_rays, int32_t n_models, int32_t n_points, int32_t* items,
+                             int32_t capacity, int32_t* n_items) {
+  VM_REQUIRE(model_rays && n_items && n_models >= 0, "vm_work_items: null argument");
+  VM_REQUIRE(n_points >= 1 && n_points <= kSB, "vm_work_items: points per ray must be in [1, 32]");
+  const int G = kSB / n_points, chunk = chunk_blocks();
+  int64_t n = 0;
+  for (int k = 0; k < n_models; ++k) {
+    VM_REQUIRE(model_rays[k] >= 0, "vm_work_items: negative ray count");
+    const int nblk = (model_rays[k] + G - 1) / G;
+    const int pk = std::max(1, (nblk + chunk - 1) / chunk);
+    for (int c = 0; c < pk; ++c, ++n) {
+      if (items && n < capacity) {
+        items[2 * n] = k;
+        items[2 * n + 1] = c;
+      }
+    }
+  }
+  VM_REQUIRE(n <= INT32_MAX, "vm_work_items: too many items");
+  *n_items = int32_t(n);
+  VM_REQUIRE(!items || n <= capacity, "vm_work_items: capacity too small");
+  return VM_OK;
+}
+
 extern "C" size_t vm_train_workspace_bytes(const VmStack* stacks, const VmBatch* batches, int n_stacks) {
   TrainPlan pl;
   if (plan_train(stacks, batches, n_stacks, pl)) return 0;
@@ -859,13 +887,21 @@ extern "C" int vm_train_step(const VmStack* stacks, const VmBatch* batches, int 
   int ff_grid = 0;
   for (int i = 0; i < n_stacks; ++i) {
     if (pl.kp.s[i].tc) continue;
-    kf.s[kf.n_stacks] = pl.kp.s[i];
-    kf.s[kf.n_stacks].item_base = ff_grid;
-    ff_grid += pl.kp.s[i].K * pl.kp.s[i].P;
-    kf.n_stacks++;
+    kf.s[kf.n_stacks++] = pl.kp.s[i];
   }
   KernelFn fn = nullptr;
   const bool use_kf32 = kf.n_stacks > 0 && kf32_enabled() && kf32_supported(kf);
+  for (int i = 0; i < kf.n_stacks; ++i) {
+    KStack& ks = kf.s[i];
+    // only the specialised kernel walks work-item tables; the generic one
+    // trains the padding rows too (zero rows: identical results)
+    if (!use_kf32) {
+      ks.items = nullptr;
+      ks.n_items = 0;
+    }
+    ks.item_base = ff_grid;
+    ff_grid += ks.items ? ks.n_items : ks.K * ks.P;
+  }
   if (kf.n_stacks > 0 && !use_kf32) {
     fn = pick_kernel<kTrain>(kf.s[0].H, kf.s[0].L, kf.n_stacks > 1 ? kf.s[1].H : 0, kf.n_stacks > 1 ? kf.s[1].L : 0);
   }

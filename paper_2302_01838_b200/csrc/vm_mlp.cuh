@@ -58,6 +58,10 @@ struct KStack {
   int tc;                     // 1: trained by the tensor-core kernel KT (vm_tc_mlp.cuh)
   int64_t N;                  // samples per model (forward/backward modes)
   int model_base;             // global model index of model 0 (losses/status)
+  int chunk;                  // ray blocks per work item (FFMA kernels)
+  const int* model_rays;      // [K] live rays per model (config 3), or null: all R
+  const int* items;           // [2*n_items] (model, chunk) work items, or null: item = k*P + chunk
+  int n_items;
   int item_base;              // first CTA index of this stack
   const float* params;
   const uint8_t* frozen;
@@ -332,9 +336,13 @@ __device__ inline void finalize_model(const KStack& st, int k, bool all_finite, 
   // stage the per-ray terms in smem (coalesced), then 3 threads sum them in
   // numpy's pairwise order without a global-load latency per add
   const float* terms = st.ray_terms + int64_t(k) * st.R * 3;
+  // rows past the model's live ray count are zero padding (config 3): their
+  // terms are 0 in the reference's sums (render.py:301-308); kernels that skip
+  // them never write these slots
+  const int live3 = 3 * (st.model_rays ? min(st.model_rays[k], st.R) : st.R);
   const bool staged = st.R * 3 <= scratch_floats;
   if (staged) {
-    for (int i = tid; i < st.R * 3; i += blockDim.x) scratch[i] = __ldcg(terms + i);
+    for (int i = tid; i < st.R * 3; i += blockDim.x) scratch[i] = i < live3 ? __ldcg(terms + i) : 0.f;
     __syncthreads();
   }
   // more than one pairwise leaf: the leaves (<= 128 rays each) are summed by
@@ -364,7 +372,8 @@ __device__ inline void finalize_model(const KStack& st, int k, bool all_finite, 
   } else if (tid < 3) {
     const int j = tid;
     const float sum = staged ? pairwise_sum([&](int64_t r) { return scratch[r * 3 + j]; }, st.R)
-                             : pairwise_sum([&](int64_t r) { return __ldcg(terms + r * 3 + j); }, st.R);
+                             : pairwise_sum([&](int64_t r) { return r * 3 < live3 ? __ldcg(terms + r * 3 + j) : 0.f; },
+                                            st.R);
     st.losses[int64_t(k) * 3 + j] = sum;
     if (!isfinite(sum)) atomicMin(&st.status[1], k);
   }

@@ -259,6 +259,9 @@ constexpr int kST = 256;
 constexpr int kRT = 128;  // per-ray kernel block size
 
 __device__ __forceinline__ bool object_live(const VmSampleObject& ob) { return ob.active && ob.n_kf > 0; }
+__device__ __forceinline__ int object_rays(const VmSampleObject& ob, const VmSampleParams& P) {
+  return (ob.n_rays > 0 && ob.n_rays < P.n_rays) ? ob.n_rays : P.n_rays;
+}
 
 // ---- per object: stream seeds, keyframe index per ray, normal resolution.
 __global__ void __launch_bounds__(kST) sample_prep_kernel(const __grid_constant__ KS ks) {
@@ -273,7 +276,9 @@ __global__ void __launch_bounds__(kST) sample_prep_kernel(const __grid_constant_
   const VmSampleObject ob = ks.objs[k];
   if (!object_live(ob)) return;
   const VmSampleParams& P = ks.p;
-  const int R = P.n_rays, nc = P.n_stratified, N = ks.N, W = ks.W;
+  // rays this object draws (config 3: fewer than the batch width; the PIXELS
+  // and SAMPLES streams are laid out for exactly this many draws)
+  const int R = object_rays(ob, P), nc = P.n_stratified, N = P.n_surface * R, W = ks.W;
 
   double* xs = reinterpret_cast<double*>(sm);                  // [W]
   double* ov_val = xs + W;                                     // [SC]
@@ -301,7 +306,7 @@ __global__ void __launch_bounds__(kST) sample_prep_kernel(const __grid_constant_
   }
 
   // ---------------- keyframe index per ray (objects.py:336) ----------------
-  int* kf_out = ks.kf + int64_t(k) * R;
+  int* kf_out = ks.kf + int64_t(k) * P.n_rays;
   const int n_kf = ob.n_kf;
   if (n_kf == 1) {
     for (int r = tid; r < R; r += kST) kf_out[r] = 0;
@@ -422,7 +427,7 @@ __global__ void __launch_bounds__(kST) sample_prep_kernel(const __grid_constant_
     }
     __syncthreads();
   }
-  double* nrm = ks.nrm + int64_t(k) * N;
+  double* nrm = ks.nrm + int64_t(k) * ks.N;
   if (s_flag & 2) {
     if (tid == 0) {  // window overflow (practically unreachable): sequential replay
       u128 s = smp.at(nbase);
@@ -487,7 +492,9 @@ __global__ void __launch_bounds__(kRT) sample_rays_kernel(const __grid_constant_
   if (rg >= int64_t(n_objects) * R) return;
   const int k = int(rg / R), r = int(rg % R);
   const VmSampleObject& ob = ks.objs[k];
-  if (!object_live(ob)) {  // zero batch (trainer.py:190-200, :272-273)
+  // zero batch (trainer.py:190-200, :272-273); rows past the object's own
+  // ray count are the same zero rows (config-3 padding, ray_ok = 0)
+  if (!object_live(ob) || r >= object_rays(ob, P)) {
     for (int i = 0; i < S; ++i) {
       ks.t32[rg * S + i] = 0.f;
       if (ks.points)
@@ -639,7 +646,7 @@ __global__ void __launch_bounds__(kRT) sample_rays_kernel(const __grid_constant_
 // one thread per (sample, band); band -1 writes the raw point.
 __global__ void encode_kernel(int64_t n_samples, int n_freq, int include, int D, int S, int64_t samples_per_obj,
                               const VmSampleObject* __restrict__ objs, const double* __restrict__ p64,
-                              float* __restrict__ enc) {
+                              float* __restrict__ enc, int R) {
   const int nb = n_freq + (include ? 1 : 0);
   const int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   if (idx >= n_samples * nb) return;
@@ -647,7 +654,8 @@ __global__ void encode_kernel(int64_t n_samples, int n_freq, int include, int D,
   const int b = int(idx % nb) - (include ? 1 : 0);
   float* out = enc + smp * D;
   const int64_t obj = smp / samples_per_obj;
-  const bool live = objs[obj].active && objs[obj].n_kf > 0;
+  const int nr = (objs[obj].n_rays > 0 && objs[obj].n_rays < R) ? objs[obj].n_rays : R;
+  const bool live = objs[obj].active && objs[obj].n_kf > 0 && (smp % samples_per_obj) / S < nr;
   const double* p = p64 + smp * 3;
   if (b < 0) {
     for (int c = 0; c < 3; ++c) out[c] = live ? float(p[c]) : 0.f;
@@ -799,7 +807,7 @@ extern "C" int vm_sample(const VmSampleObject* objects, int n_objects, const VmK
     const int nb = p.n_freq + (p.include_input ? 1 : 0);
     const int64_t work = n * nb;
     encode_kernel<<<unsigned((work + 255) / 256), 256, 0, s>>>(n, p.n_freq, p.include_input, D, pl.S, spo, objects,
-                                                               ks.p64, const_cast<float*>(out->encoded));
+                                                               ks.p64, const_cast<float*>(out->encoded), p.n_rays);
     VM_CUDA(cudaGetLastError());
     vm_profile_count_kernels(1);
   }

@@ -60,7 +60,7 @@ class KeyframeArena:
 
 KF_DTYPE = np.dtype([("texel_off", "<i8"), ("bbox", "<i4", 4), ("pose", "<f8", 12)])
 OBJ_DTYPE = np.dtype([("object_id", "<i8"), ("kf_begin", "<i4"), ("n_kf", "<i4"), ("active", "<i4"),
-                      ("reserved", "<i4"), ("box_min", "<f8", 3), ("box_max", "<f8", 3), ("center", "<f8", 3),
+                      ("n_rays", "<i4"), ("box_min", "<f8", 3), ("box_max", "<f8", 3), ("center", "<f8", 3),
                       ("half", "<f8", 3), ("pe_scale", "<f8")])
 assert KF_DTYPE.itemsize == C.sizeof(_lib.VmKeyframe) and OBJ_DTYPE.itemsize == C.sizeof(_lib.VmSampleObject)
 
@@ -114,7 +114,7 @@ def build_tables(arena: KeyframeArena, instances, bound_pad: float, frozen=None,
     n = len(instances)
     objs = np.zeros(max(n, 1), OBJ_DTYPE)
     parts = []
-    n_kf, mins, maxs, ids, active, scale = [], [], [], [], [], []
+    n_kf, mins, maxs, ids, active, scale, rays = [], [], [], [], [], [], []
     for k, inst in enumerate(instances):
         kfs = inst.keyframes
         for kf in kfs:
@@ -127,6 +127,7 @@ def build_tables(arena: KeyframeArena, instances, bound_pad: float, frozen=None,
         ids.append(inst.object_id)
         active.append(1 if (inst.active and not (frozen is not None and frozen[k])) else 0)
         scale.append(inst.pe_scale)
+        rays.append(int(getattr(inst, "n_rays", None) or 0))
     if n:  # one vectorised fill per field (per-instance numpy scalar stores were the cost)
         nk = np.asarray(n_kf, np.int32)
         objs["n_kf"][:n] = nk
@@ -134,6 +135,7 @@ def build_tables(arena: KeyframeArena, instances, bound_pad: float, frozen=None,
         objs["object_id"][:n] = ids
         objs["active"][:n] = active
         objs["pe_scale"][:n] = scale
+        objs["n_rays"][:n] = rays
         mins = np.asarray(mins, np.float64).reshape(n, 3)
         maxs = np.asarray(maxs, np.float64).reshape(n, 3)
         pad = bound_pad * (0.5 * (maxs - mins))
@@ -179,6 +181,8 @@ class SampleBuffers:
         self.target_mask = b(K, R)
         self.valid_depth = b(K, R)
         self.ray_ok = b(K, R)
+        self.model_rays = None   # [K] int32 live rays per model (config 3), or None
+        self.work_items = None   # [2*n] int32 (model, chunk) items of the object kernel
         self.aux = None
         if aux:
             i64 = lambda *s: torch.zeros(s, dtype=torch.int64, device=device)
@@ -199,7 +203,27 @@ class SampleBuffers:
         out.target_mask = self.target_mask.data_ptr()
         out.valid_depth = self.valid_depth.data_ptr()
         out.ray_ok = self.ray_ok.data_ptr()
+        if self.model_rays is not None:
+            out.model_rays = self.model_rays.data_ptr()
+            out.work_items = self.work_items.data_ptr()
+            out.n_work_items = self.work_items.numel() // 2
         return out
+
+    def set_model_rays(self, rays, device) -> None:
+        """Per-model live ray counts (host ints, <= R) and the object kernel's
+        work items for them; all-equal-to-R clears both (uniform batch)."""
+        rays = np.minimum(np.asarray(rays, np.int32), self.R)
+        if len(rays) == 0 or (rays == self.R).all():
+            self.model_rays = self.work_items = None
+            return
+        lib = _lib.load()
+        cnt = C.c_int32()
+        _lib.check(lib.vm_work_items(rays.ctypes.data, len(rays), self.S, None, 0, C.byref(cnt)), "vm_work_items")
+        items = np.zeros(2 * max(cnt.value, 1), np.int32)
+        _lib.check(lib.vm_work_items(rays.ctypes.data, len(rays), self.S, items.ctypes.data, cnt.value,
+                                     C.byref(cnt)), "vm_work_items")
+        self.model_rays = torch.from_numpy(rays.copy()).to(device)
+        self.work_items = torch.from_numpy(items[:2 * cnt.value].copy()).to(device)
 
 
 def run_sampler(arena: KeyframeArena, kf_table: torch.Tensor, obj_table: torch.Tensor, n_objects: int,

@@ -80,7 +80,7 @@ class Mapper:
         return self.map.add_background(aabb, scale, idx)
 
     def add_object(self, semantic_class: int, aabb, pe_scale: float | None = None, object_id: int | None = None,
-                   init_index: int | None = None):
+                   init_index: int | None = None, n_rays: int | None = None):
         """append_model + ObjectMap.add_object + model_to_object (trainer.py:254-256).
 
         `object_id` / `init_index` place a shard of a global map: the object
@@ -94,6 +94,10 @@ class Mapper:
                            init_index=init_index)
         scale = self.cfg.pe_scale_object if pe_scale is None else pe_scale
         inst = self.map.add_object(semantic_class, aabb, scale, idx, object_id=object_id)
+        if n_rays is not None:
+            if not 1 <= int(n_rays) <= self.cfg.rays_per_object:
+                raise ValueError(f"n_rays must be in [1, rays_per_object={self.cfg.rays_per_object}]")
+            inst.n_rays = int(n_rays)
         self.model_to_object.append(inst.object_id)
         return inst
 
@@ -148,6 +152,12 @@ class Mapper:
         if K and (self._buf_obj is None or self._buf_obj.K != K):
             self._buf_obj = SampleBuffers(K, c.rays_per_object, S, c.arch_object.input_dim, self.encode, self.device)
             self._g = None  # batch buffers reallocated: the step graphs must be recaptured
+        if K:  # per-object ray counts (config 3): live rows + the object kernel's work items
+            rays = tuple(int(i.n_rays or c.rays_per_object) for i in objs)
+            if rays != getattr(self._buf_obj, "_rays_sig", None):
+                self._buf_obj.set_model_rays(rays, self.device)
+                self._buf_obj._rays_sig = rays
+                self._g = None  # grid size / table pointers changed
         if bg is not None and self._buf_bg is None:
             self._buf_bg = SampleBuffers(1, c.rays_background, S, c.arch_background.input_dim, self.encode,
                                          self.device)
@@ -240,7 +250,8 @@ class Mapper:
         tabs = tuple(t.data_ptr() for tab in self._tables if tab is not None for t in tab)
         bufs = tuple(b.t.data_ptr() for b in (self._buf_obj, self._buf_bg) if b is not None)
         frz = tuple(p.frozen_device().data_ptr() for p in (self.obj_params, self.bg_params) if p.count)
-        return (tabs, bufs, frz, self.arena.rgbd.data_ptr(), self.arena.mask.data_ptr(),
+        rays = getattr(self._buf_obj, "_rays_sig", None)
+        return (tabs, bufs, frz, rays, self.arena.rgbd.data_ptr(), self.arena.mask.data_ptr(),
                 self.obj_params.arena.data_ptr(), self.bg_params.arena.data_ptr(),
                 self.obj_params.count, self.bg_params.count, self.cfg.train_background)
 
@@ -262,6 +273,7 @@ class Mapper:
                   ] if has_bg else [None, None]
         if objs_n:
             bufs_o[1].pe_scale.copy_(bufs_o[0].pe_scale)
+            bufs_o[1].model_rays, bufs_o[1].work_items = bufs_o[0].model_rays, bufs_o[0].work_items
         if has_bg:
             bufs_b[1].pe_scale.copy_(bufs_b[0].pe_scale)
         step_dev = torch.zeros(1, dtype=torch.int64, device=dev)

@@ -61,6 +61,10 @@ class ObjectInstance:
     active: bool = True
     obs_count: int = 0
     keyframes: list = field(default_factory=list)
+    # rays drawn per training step when fewer than TrainConfig.rays_per_object
+    # (mixed per-object ray counts, BASELINE config 3); the batch rows beyond
+    # are zero padding with ray_ok = False.  None: rays_per_object.
+    n_rays: int | None = None
 
     def padded_aabb(self, fraction: float) -> AABB:
         return self.aabb.padded(fraction)

@@ -52,8 +52,12 @@ def config(name: str) -> dict:
         return make_scene(3, n_kf=2, width=160, height=120, focal=100.0, crop=(20, 60), n_kf_bg=2, seed=1)
     if name in ("2", "5"):
         return make_scene(50, n_kf=5, seed=0)
-    if name == "3":
-        return make_scene(200, n_kf=10, seed=3)
+    if name == "3":   # load-imbalance stress: per-object rays log-uniform in [30, 480]
+        sc = make_scene(200, n_kf=10, seed=3)
+        g = np.random.default_rng(33)
+        for ob, r in zip(sc["objects"], np.exp(g.uniform(np.log(30), np.log(480), len(sc["objects"])))):
+            ob["n_rays"] = int(round(r))
+        return sc
     if name == "4":
         return make_scene(1000, n_kf=5, seed=4)
     raise KeyError(f"unknown config {name!r}")
@@ -75,9 +79,9 @@ def populate(mapper, scene: dict, objects=None, with_background: bool = True) ->
         if objects is not None and i not in objects:
             continue
         if objects is None:
-            inst = mapper.add_object(1, ob["aabb"])
+            inst = mapper.add_object(1, ob["aabb"], n_rays=ob.get("n_rays"))
         else:
-            inst = mapper.add_object(1, ob["aabb"], object_id=i + 1, init_index=i)
+            inst = mapper.add_object(1, ob["aabb"], object_id=i + 1, init_index=i, n_rays=ob.get("n_rays"))
         for kf in ob["keyframes"]:
             mapper.add_keyframe(inst, kf["frame_id"], kf["pose"], kf["bbox"], kf["mask"], scene["rgb"],
                                 scene["depth"])

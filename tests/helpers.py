@@ -197,7 +197,7 @@ def oracle_mapstate(scene, cfg, obj_hidden=32, bg_hidden=128, objects=None, with
         if objects is not None and i not in objects:
             continue
         objs.append(_NS(object_id=i + 1, keyframes=kfs(spec), aabb=spec["aabb"], pe_scale=cfg.pe_scale_object,
-                        active=True, model_index=len(objs)))
+                        active=True, model_index=len(objs), n_rays=spec.get("n_rays")))
         keys.append(i)
     bg = None
     if scene["background"] is not None and with_background:

@@ -97,4 +97,5 @@ def test_sharded_shard_matches_oracle_shard(cuda):
                                                                ([0] if rank == shard.background_rank else []))
             for oid, trip in exp.items():
                 np.testing.assert_allclose(np.array(rep.losses[oid]), np.array(trip), rtol=1e-4, atol=1e-5)
-        assert_params_close(m.obj_params, ms.obj)
+        if m.obj_params.count:  # the background's rank may own no objects
+            assert_params_close(m.obj_params, ms.obj)

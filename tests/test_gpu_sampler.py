@@ -27,8 +27,16 @@ def _check_stack(mapper, ms, step, background):
     R = ms.rays_background if background else ms.rays_object
     enc_mismatch = 0
     for k, inst in enumerate(insts):
-        exp, aux = O.assemble_batch(inst, ms.intr, arch, R, step, ms.seed, ms.sampling, ms.bound_pad,
+        nr = O.object_rays(inst, R)  # config 3: rows >= nr are zero padding
+        exp, aux = O.assemble_batch(inst, ms.intr, arch, nr, step, ms.seed, ms.sampling, ms.bound_pad,
                                     with_aux=True)
+        exp = O.pad_batch(exp, R, ms.sampling.n_stratified + ms.sampling.n_surface, arch.input_dim)
+        if nr < R:
+            for key in ("kf_idx", "u", "v", "t64"):
+                assert not buf.aux[key][k][nr:].any()
+            aux = dict(aux, t64=np.concatenate([aux["t64"], np.zeros((R - nr,) + aux["t64"].shape[1:])]))
+            for key in ("kf_idx", "u", "v"):
+                aux[key] = np.concatenate([aux[key], np.zeros(R - nr, aux[key].dtype)])
         np.testing.assert_array_equal(buf.aux["kf_idx"][k].cpu().numpy(), aux["kf_idx"])
         np.testing.assert_array_equal(buf.aux["u"][k].cpu().numpy(), aux["u"])
         np.testing.assert_array_equal(buf.aux["v"][k].cpu().numpy(), aux["v"])

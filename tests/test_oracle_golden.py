@@ -129,3 +129,24 @@ def test_train_on_batch_matches_reference(tag, arch, k, rays, pts):
     ls = np.array([O.train_on_batch(st, b) for _ in range(20)])
     np.testing.assert_allclose(ls, gold[f"{tag}_losses"], rtol=1e-6, atol=1e-7)
     _blas_close(_flat(st), gold[f"{tag}_params"])
+
+
+def test_padding_rows_are_inert():
+    """Config 3 semantics: zero-batch rows (ray_ok = False) appended to an
+    object's batch change neither its losses nor its parameter update
+    (render.py:301-333 masks them out of every term)."""
+    from paper_2302_01838_b200 import TrainConfig
+    from paper_2302_01838_b200.scenes import make_scene
+    from tests.helpers import oracle_mapstate
+    sc = make_scene(2, n_kf=2, width=160, height=120, focal=100.0, crop=(20, 60), n_kf_bg=1, seed=4)
+    cfg = TrainConfig(rays_per_object=40, train_background=False)
+    a, b = oracle_mapstate(sc, cfg), oracle_mapstate(sc, cfg)
+    for inst in b.objects:
+        inst.n_rays = 25
+    b.rays_object = 40
+    a.rays_object = 25
+    la, lb = O.map_update_step(a), O.map_update_step(b)
+    for oid in la:
+        np.testing.assert_allclose(la[oid], lb[oid], rtol=1e-6, atol=1e-7)
+    for l in range(len(a.obj.W)):
+        np.testing.assert_allclose(a.obj.W[l][:2], b.obj.W[l][:2], rtol=1e-6, atol=1e-7)

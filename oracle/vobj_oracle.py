@@ -564,3 +564,133 @@ def map_update_step(ms: MapState) -> dict:
         out[0] = tuple(float(x) for x in vals)
     ms.global_step += 1
     return out
+
+
+# --------------------------------------------------------------------------
+# forward-only inference (meshing.py) -- SURVEY 8f #1
+# --------------------------------------------------------------------------
+
+def _model_view(st: Stack, index: int) -> Stack:
+    """StackedModelParams.model_view (models.py:90-98): one model as a stack."""
+    v = st.copy()
+    v.W = [w[index:index + 1] for w in st.W]
+    v.b = [b[index:index + 1] for b in st.b]
+    v.count = 1
+    return v
+
+
+def query_grid(st: Stack, model_index: int, bmin, bmax, pe_scale: float, resolution, chunk=None) -> np.ndarray:
+    """meshing.py:64-97: occupancy on np.linspace grids (meshgrid 'ij'),
+    f32 points encoded in f32 and run through the forward pass in chunks."""
+    if isinstance(resolution, int):
+        resolution = (resolution,) * 3
+    if any(r < 2 for r in resolution):
+        raise ValueError(f"grid resolution must be >= 2 per axis, got {resolution}")
+    bmin, bmax = np.asarray(bmin, np.float64), np.asarray(bmax, np.float64)
+    center, half = 0.5 * (bmin + bmax), 0.5 * (bmax - bmin)
+    axes = [np.linspace(bmin[i], bmax[i], resolution[i]) for i in range(3)]
+    view = _model_view(st, model_index)
+    if chunk is None:
+        chunk = 65536 if st.arch.hidden <= 64 else 16384
+    n = int(np.prod(resolution))
+    out = np.empty(n, np.float32)
+    gx, gy, gz = np.meshgrid(*axes, indexing="ij")
+    pts = np.stack([gx, gy, gz], axis=-1).reshape(-1, 3)
+    for a in range(0, n, chunk):
+        b = min(a + chunk, n)
+        enc = positional_encode(pts[a:b].astype(np.float32), center, half, st.arch, pe_scale)
+        occ, _, _, _ = mlp_forward(view, enc[None])
+        out[a:b] = occ[0]
+    return out.reshape(resolution)
+
+
+def eval_field(st: Stack, model_index: int, bmin, bmax, pe_scale: float, points, chunk: int):
+    """meshing.py:453-476 -> occupancy [N,S], colour [N,S,3]."""
+    bmin, bmax = np.asarray(bmin, np.float64), np.asarray(bmax, np.float64)
+    center, half = 0.5 * (bmin + bmax), 0.5 * (bmax - bmin)
+    view = _model_view(st, model_index)
+    n, s, _ = points.shape
+    occ = np.empty((n, s), np.float32)
+    col = np.empty((n, s, 3), np.float32)
+    rows = max(1, chunk // max(s, 1))
+    for a in range(0, n, rows):
+        b = min(a + rows, n)
+        enc = positional_encode(points[a:b].astype(np.float32), center, half, st.arch, pe_scale)
+        o, c, _, _ = mlp_forward(view, enc.reshape(1, -1, enc.shape[-1]))
+        occ[a:b] = o.reshape(b - a, s)
+        col[a:b] = c.reshape(b - a, s, 3)
+    return occ, col
+
+
+def _midpoints(lo, hi, n):
+    """meshing.py:479-482."""
+    centres = (np.arange(n) + 0.5) / n
+    return lo[:, None] + centres * (hi - lo)[:, None]
+
+
+def _padded(bmin, bmax, fraction):
+    bmin, bmax = np.asarray(bmin, np.float64), np.asarray(bmax, np.float64)
+    pad = fraction * (0.5 * (bmax - bmin))
+    return bmin - pad, bmax + pad
+
+
+def render_view(obj: Stack, bg: Stack, objects, background, intr, pose, t_near=0.0, t_far=8.0,
+                samples_object=48, samples_background=48, samples_refine=32, refine_window=0.25,
+                bound_pad=0.10, threshold=0.5, chunk=65536):
+    """meshing.py:485-579.  `objects`: instances (object_id, aabb, pe_scale,
+    model_index) in ascending id order; `background` likewise.
+    Returns (rgb [H,W,3] f32, depth [H,W] f32, instance [H,W] i32)."""
+    w, h = intr.width, intr.height
+    uu, vv = np.meshgrid(np.arange(w), np.arange(h))
+    pix = np.stack([uu.ravel(), vv.ravel()], axis=1).astype(np.float64)
+    n_pix = pix.shape[0]
+    d_cam = np.empty((n_pix, 3))
+    d_cam[:, 0] = (pix[:, 0] - intr.cx) / intr.fx
+    d_cam[:, 1] = (pix[:, 1] - intr.cy) / intr.fy
+    d_cam[:, 2] = 1.0
+    scale = np.linalg.norm(d_cam, axis=-1)
+    pose = np.asarray(pose, np.float64)
+    dirs = d_cam @ pose[:3, :3].T
+    dirs /= np.linalg.norm(dirs, axis=-1, keepdims=True)
+    origins = np.broadcast_to(pose[:3, 3], dirs.shape)
+    bmin, bmax = _padded(background.aabb.min, background.aabb.max, bound_pad)
+    t_bg = _midpoints(np.full(n_pix, t_near), np.full(n_pix, t_far), samples_background)
+    occ, col = eval_field(bg, background.model_index, bmin, bmax, background.pe_scale,
+                          origins[:, None, :] + t_bg[:, :, None] * dirs[:, None, :], chunk)
+    c_op, c_dep, c_col, _, _ = render_forward(occ, col, t_bg)
+    if samples_refine > 0:
+        centre = np.clip(c_dep, t_near + refine_window, t_far - refine_window)
+        lo_r = np.maximum(centre - refine_window, t_near)
+        hi_r = np.minimum(centre + refine_window, t_far)
+        t_r = _midpoints(lo_r, hi_r, samples_refine)
+        occ, col = eval_field(bg, background.model_index, bmin, bmax, background.pe_scale,
+                              origins[:, None, :] + t_r[:, :, None] * dirs[:, None, :], chunk)
+        _, r_dep, r_col, _, _ = render_forward(occ, col, t_r)
+        use = c_op >= 0.5
+        bg_depth = np.where(use, r_dep, c_dep)
+        bg_col = np.where(use[:, None], r_col, c_col)
+    else:
+        bg_depth, bg_col = c_dep, c_col
+    depth = bg_depth.astype(np.float64)
+    colour = bg_col.astype(np.float64)
+    instance = np.zeros(n_pix, np.int32)
+    best = np.full(n_pix, np.inf)
+    for inst in objects:
+        omin, omax = _padded(inst.aabb.min, inst.aabb.max, bound_pad)
+        t0, t1, hit = ray_box(origins, dirs, omin, omax)
+        t0 = np.maximum(t0, t_near)
+        sel = np.flatnonzero(hit & (t1 > t0))
+        if sel.size == 0:
+            continue
+        t_o = _midpoints(t0[sel], t1[sel], samples_object)
+        occ, col = eval_field(obj, inst.model_index, omin, omax, inst.pe_scale,
+                              origins[sel, None, :] + t_o[:, :, None] * dirs[sel, None, :], chunk)
+        op, dep, cl, _, _ = render_forward(occ, col, t_o)
+        win = (op >= threshold) & (dep < best[sel])
+        gi = sel[win]
+        best[gi] = dep[win]
+        depth[gi] = dep[win]
+        colour[gi] = cl[win]
+        instance[gi] = inst.object_id
+    return (np.clip(colour, 0.0, 1.0).reshape(h, w, 3).astype(np.float32),
+            (depth / scale).reshape(h, w).astype(np.float32), instance.reshape(h, w))

@@ -160,11 +160,28 @@ def main():
         tr[f"{tag}_losses"] = np.array(ls)
         tr[f"{tag}_params"] = flat(p)
     np.savez_compressed(HERE / "train_cfg1.npz", **tr)
+
+    # ---- forward-only inference on the trained config-1 map (meshing.py) ----
+    from vobj.meshing import query_grid, render_view
+    from vobj.render import CameraIntrinsics
+    inf = {}
+    o0 = m.instance_for_model(0)
+    inf["grid_obj0"] = query_grid(m.obj_params, 0, o0.aabb.padded(0.10), o0.pe_scale, (9, 10, 11)).values
+    bgi = m.map.background
+    inf["grid_bg"] = query_grid(m.bg_params, bgi.model_index, bgi.aabb.padded(0.10), bgi.pe_scale, 8).values
+    intr = scene["intrinsics"]
+    ri = CameraIntrinsics(intr.fx, intr.fy, intr.cx, intr.cy, intr.width, intr.height)
+    pose = scene["background"]["keyframes"][0]["pose"]
+    for tag, thr in (("v", 0.5), ("v0", 0.0)):
+        view = render_view(m.obj_params, m.bg_params, m.map, ri, pose, samples_object=16, samples_background=16,
+                           samples_refine=8, threshold=thr)
+        inf[tag + "_rgb"], inf[tag + "_depth"], inf[tag + "_inst"] = view.rgb, view.depth, view.instance
+    np.savez_compressed(HERE / "infer_cfg1.npz", **inf)
     import numpy
     (HERE / "PROVENANCE.txt").write_text(
         "Generated by tests/golden/make_golden.py from the reference at /root/reference/pkg/src\n"
         f"numpy {numpy.__version__}; scipy {__import__('scipy').__version__}\n")
-    for f in ("ops.npz", "sampler_cfg1.npz", "train_cfg1.npz"):
+    for f in ("ops.npz", "sampler_cfg1.npz", "train_cfg1.npz", "infer_cfg1.npz"):
         print(f, (HERE / f).stat().st_size)
 
 

@@ -215,3 +215,43 @@ def oracle_mapstate(scene, cfg, obj_hidden=32, bg_hidden=128, objects=None, with
     return O.MapState(intr=intr, objects=objs, background=bg, obj=ost, bg=bst, seed=cfg.seed,
                       rays_object=cfg.rays_per_object, rays_background=cfg.rays_background, sampling=samp,
                       bound_pad=cfg.association.bound_pad, train_background=cfg.train_background)
+
+
+def load_flat_oracle(st: O.Stack, flat: np.ndarray) -> None:
+    """Inverse of flat_oracle: per model [W0, b0, W1, b1, ...] rows."""
+    k = flat.shape[0]
+    off = 0
+    for l in range(len(st.W)):
+        fo, fi = st.W[l].shape[1:]
+        st.W[l][:k] = flat[:, off:off + fo * fi].reshape(k, fo, fi)
+        off += fo * fi
+        st.b[l][:k] = flat[:, off:off + fo]
+        off += fo
+
+
+def load_flat_params(params, flat: np.ndarray) -> None:
+    """Write [K, P] flat reference parameters into a device stack's views."""
+    import torch
+    k = flat.shape[0]
+    off = 0
+    for l in range(len(params.weights)):
+        fo, fi = params.weights[l].shape[1:]
+        params.weights[l][:k].copy_(torch.from_numpy(flat[:, off:off + fo * fi].reshape(k, fo, fi).astype(np.float32)))
+        off += fo * fi
+        params.biases[l][:k].copy_(torch.from_numpy(flat[:, off:off + fo].astype(np.float32)))
+        off += fo
+    params.version += 1
+
+
+def trained_config1_oracle():
+    """Config-1 oracle map state carrying the reference's parameters after
+    its 20 training steps (tests/golden/train_cfg1.npz)."""
+    from pathlib import Path
+    from paper_2302_01838_b200 import TrainConfig
+    from paper_2302_01838_b200.scenes import config
+    scene = config("1")
+    ms = oracle_mapstate(scene, TrainConfig())
+    gold = np.load(Path(__file__).resolve().parent / "golden" / "train_cfg1.npz")
+    load_flat_oracle(ms.obj, gold["obj_params"])
+    load_flat_oracle(ms.bg, gold["bg_params"])
+    return scene, ms, gold

@@ -20,7 +20,8 @@ from paper_2302_01838_b200 import TrainConfig
 from paper_2302_01838_b200.mapper import Mapper
 from paper_2302_01838_b200.scenes import config, make_scene, populate
 
-from .helpers import assert_params_close, oracle_mapstate
+from .helpers import (assert_step_close, f64_batch, f64_stack, flat_oracle, flat_params, oracle_from_gpu,
+                      oracle_mapstate, rel_l2)
 from .test_gpu_sampler import _check_stack
 
 pytestmark = pytest.mark.gpu
@@ -47,19 +48,41 @@ def test_config3_sampler_bit_exact(cuda, step):
 @pytest.mark.parametrize("train_background", [False, True])
 def test_config3_mapper_5_steps(cuda, train_background):
     scene, cfg = _mixed_scene()
+    R = cfg.rays_per_object
     cfg = TrainConfig(rays_per_object=cfg.rays_per_object, rays_background=cfg.rays_background,
                       train_background=train_background)
     m = Mapper(scene["intrinsics"], cfg)
     populate(m, scene)
     ms = oracle_mapstate(scene, cfg)
+    pts = cfg.points_per_ray
     for s in range(5):
+        # teacher-forced reference step (f32 and f64) from the GPU's state on
+        # the same padded batch: the per-component contract of test_gpu_config2
+        fo = oracle_from_gpu(m.obj_params, m.obj_state, ms.obj)
+        fo64 = f64_stack(fo)
+        bo = O.stack_batches([O.pad_batch(O.assemble_batch(inst, ms.intr, ms.obj.arch, O.object_rays(inst, R),
+                                                           ms.global_step, ms.seed, ms.sampling, ms.bound_pad),
+                                          R, pts, ms.obj.arch.input_dim) for inst in ms.objects])
+        lo = O.train_on_batch(fo, bo)
+        O.train_on_batch(fo64, f64_batch(bo))
         rep = m.train_step()
         exp = O.map_update_step(ms)
         assert sorted(rep.losses) == sorted(exp)
         for oid, trip in exp.items():
             np.testing.assert_allclose(np.array(rep.losses[oid]), np.array(trip), rtol=1e-4, atol=1e-5,
                                        err_msg=f"step {s} object {oid}")
-    assert_params_close(m.obj_params, ms.obj)
+        for k, oid in enumerate(m.model_to_object):
+            np.testing.assert_allclose(np.array(rep.losses[oid]), [lo[0][k], lo[1][k], lo[2][k]], rtol=1e-4,
+                                       atol=1e-5)
+        # objects drawing 1-5 rays have weight-gradient components that are
+        # sums of <= 50 terms cancelling to ~0; a different f32 summation
+        # order (the reference's BLAS vs the kernel's register tiles) can flip
+        # their sign, which Adam's first steps turn into +-lr.  So a handful
+        # of components (<= 2e-4 of the stack) may sit off both bands while
+        # every model stays within 5e-5 relative L2 of the reference step.
+        assert_step_close(m.obj_params, m.obj_state, fo, fo64, name=f"step {s} objects", max_off_frac=2e-4,
+                          param_rel_l2=5e-5)
+    assert rel_l2(flat_params(m.obj_params), flat_oracle(ms.obj)).max() <= 1e-4
 
 
 def test_config3_full_size_2_steps(cuda):
@@ -76,4 +99,6 @@ def test_config3_full_size_2_steps(cuda):
         for oid, trip in exp.items():
             np.testing.assert_allclose(np.array(rep.losses[oid]), np.array(trip), rtol=1e-4, atol=1e-5,
                                        err_msg=f"step {s} object {oid}")
-    assert_params_close(m.obj_params, ms.obj)
+    e = rel_l2(flat_params(m.obj_params), flat_oracle(ms.obj))
+    print(f"config 3: per-object rel L2 after 2 steps: max {e.max():.2e}")
+    assert e.max() <= 1e-4

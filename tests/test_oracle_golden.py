@@ -150,3 +150,24 @@ def test_padding_rows_are_inert():
         np.testing.assert_allclose(la[oid], lb[oid], rtol=1e-6, atol=1e-7)
     for l in range(len(a.obj.W)):
         np.testing.assert_allclose(a.obj.W[l][:2], b.obj.W[l][:2], rtol=1e-6, atol=1e-7)
+
+
+def test_inference_matches_reference():
+    """query_grid (meshing.py:64-97) and render_view (meshing.py:485-579) of
+    the oracle on the reference's trained config-1 map vs the reference."""
+    from tests.helpers import trained_config1_oracle
+    scene, ms, _ = trained_config1_oracle()
+    gold = np.load(G / "infer_cfg1.npz")
+    o0 = ms.objects[0]
+    bmin, bmax = O._padded(o0.aabb.min, o0.aabb.max, 0.10)
+    _blas_close(O.query_grid(ms.obj, 0, bmin, bmax, o0.pe_scale, (9, 10, 11)), gold["grid_obj0"])
+    bg = ms.background
+    bmin, bmax = O._padded(bg.aabb.min, bg.aabb.max, 0.10)
+    _blas_close(O.query_grid(ms.bg, 0, bmin, bmax, bg.pe_scale, 8), gold["grid_bg"])
+    pose = scene["background"]["keyframes"][0]["pose"]
+    for tag, thr in (("v", 0.5), ("v0", 0.0)):
+        rgb, depth, inst = O.render_view(ms.obj, ms.bg, ms.objects, bg, ms.intr, pose, samples_object=16,
+                                         samples_background=16, samples_refine=8, threshold=thr)
+        _blas_close(rgb, gold[tag + "_rgb"])
+        _blas_close(depth, gold[tag + "_depth"])
+        np.testing.assert_array_equal(inst, gold[tag + "_inst"])

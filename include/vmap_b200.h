@@ -228,6 +228,43 @@ int vm_sample(const VmSampleObject* objects /* device [K] */, int n_objects,
               const uint8_t* mask, const VmSampleParams* params, VmBatch* out /* device ptrs */,
               VmSampleAux* aux, void* workspace, size_t workspace_bytes, void* stream);
 
+/* ---- forward-only inference (meshing.py) --------------------
+   Host pointers for the small double[3] arguments (box corners, origin);
+   device pointers for arrays.  Point sets are processed in chunks of `chunk`
+   samples through `workspace` (vm_infer_workspace_bytes(arch, chunk)). */
+size_t vm_infer_workspace_bytes(const VmArch* arch, int64_t chunk);
+/* query_grid (meshing.py:64-97): occupancy of model `model_index` on the
+   np.linspace grid over [box_min, box_max] (meshgrid 'ij', C order) ->
+   occ_out [rx*ry*rz] (device). */
+int vm_query_grid(const VmStack* stack, int32_t model_index, const double* box_min, const double* box_max,
+                  double pe_scale, const int32_t* resolution /* host [3] */, float* occ_out, void* workspace,
+                  size_t workspace_bytes, int64_t chunk, void* stream);
+/* _eval_field + render_rays (meshing.py:453-482, render.py:230-246) for rays
+   origin + t dirs[sel[r]] at the S bin midpoints of [lo[r], hi[r]] (or the
+   constants when lo/hi are NULL; sel NULL = identity) -> per ray opacity
+   (f32), depth (f64, as render_view forms it) and colour (f32). */
+int vm_eval_rays(const VmStack* stack, int32_t model_index, const double* box_min, const double* box_max,
+                 double pe_scale, const double* origin, const double* dirs, const int32_t* sel, int64_t n_rays,
+                 const double* lo, const double* hi, double lo_const, double hi_const, int32_t n_samples,
+                 float* opacity, double* depth, float* colour, void* workspace, size_t workspace_bytes,
+                 int64_t chunk, void* stream);
+/* pixel rays of a camera (meshing.py:516-526): dirs [H*W,3] f64 unit,
+   scale [H*W] = |d_cam|; intr = (fx, fy, cx, cy) host, pose 4x4 host. */
+int vm_view_rays(const double* intr, int32_t width, int32_t height, const double* pose, double* dirs,
+                 double* scale, void* stream);
+/* ray_box_intersect + render_view's t0 = max(t0, t_near), hit & t1 > t0
+   (render.py:111-139, meshing.py:562-565): compacted ray indices `sel`,
+   their [lo, hi] and the count (device int32). */
+int vm_ray_box_select(const double* origin, const double* dirs, int64_t n, const double* box_min,
+                      const double* box_max, double t_near, int32_t* sel, int32_t* count, double* lo, double* hi,
+                      void* stream);
+/* render_view's per-pixel steps (meshing.py:538-581): op 0 refine window,
+   1 background choice + state init, 2 one object's depth competition,
+   3 z-depth + clipped colour outputs (see vm_infer.cu). */
+int vm_view_compose(int32_t op, int64_t n, const void* a0, const void* a1, const void* a2, const void* a3,
+                    const void* a4, const void* a5, double p0, double p1, double p2, int32_t i0, void* o0,
+                    void* o1, void* o2, void* o3, void* stream);
+
 /* ---- profiling: event-time every fused-kernel launch of vm_train_step ---- */
 int vm_profile_enable(int on);                          /* resets the launch log */
 int vm_profile_read(int* launches, double* total_ms);   /* syncs on the events; MLP phase */

@@ -86,6 +86,18 @@ class VmSampleAux(C.Structure):
 _SIGNATURES = {
     "vm_model_layout": (C.c_int, [C.POINTER(VmArch), C.POINTER(VmLayout)]),
     "vm_train_workspace_bytes": (C.c_size_t, [C.POINTER(VmStack), C.POINTER(VmBatch), C.c_int]),
+    "vm_infer_workspace_bytes": (C.c_size_t, [C.POINTER(VmArch), C.c_int64]),
+    "vm_query_grid": (C.c_int, [C.POINTER(VmStack), C.c_int32, C.c_void_p, C.c_void_p, C.c_double, C.c_void_p,
+                                C.c_void_p, C.c_void_p, C.c_size_t, C.c_int64, C.c_void_p]),
+    "vm_eval_rays": (C.c_int, [C.POINTER(VmStack), C.c_int32, C.c_void_p, C.c_void_p, C.c_double, C.c_void_p,
+                               C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_double, C.c_double,
+                               C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_int64,
+                               C.c_void_p]),
+    "vm_view_rays": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "vm_ray_box_select": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_double,
+                                    C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "vm_view_compose": (C.c_int, [C.c_int32, C.c_int64] + [C.c_void_p] * 6 + [C.c_double] * 3 + [C.c_int32]
+                        + [C.c_void_p] * 5),
     "vm_work_items": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_int32, C.POINTER(C.c_int32)]),
     "vm_train_step": (C.c_int, [C.POINTER(VmStack), C.POINTER(VmBatch), C.c_int, VmLossWeights,
                                 C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]),

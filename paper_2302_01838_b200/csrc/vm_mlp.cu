@@ -1057,7 +1057,9 @@ int run_fwd_bwd(const VmStack* st, const float* encoded, int64_t n_samples, cons
   if (backward) {
     ks.P = 1;  // one CTA per model reduces every block of that model
   } else {
-    ks.P = std::max(1, std::min(nblk, 64));
+    // forward only (no reduction): enough CTAs to fill the GPU even for one
+    // model (inference grids / rays), >= 1 block each
+    ks.P = std::max(1, std::min(nblk, std::max(64, 148 * 8 / std::max(ks.K, 1))));
   }
   if (ks.K == 0 || n_samples == 0) {
     if (backward && ks.K > 0) VM_CUDA(cudaMemsetAsync(grads, 0, size_t(ks.K) * ks.block * 4, s));

@@ -265,6 +265,32 @@ int vm_view_compose(int32_t op, int64_t n, const void* a0, const void* a1, const
                     const void* a4, const void* a5, double p0, double p1, double p2, int32_t i0, void* o0,
                     void* o1, void* o2, void* o3, void* stream);
 
+/* ---- per-frame ingestion (trainer.py:226-265) ---------- */
+/* Dataset.frame's conversion (datasets.py:160-175) on the device: 8-bit BGR
+   -> f32 RGB / 255, 16-bit depth -> f32 / depth_scale, 16-bit ids -> int32.
+   Any of the three inputs may be NULL. */
+int vm_decode_frame(const uint8_t* bgr, const uint16_t* depth16, const uint16_t* mask16, int32_t width,
+                    int32_t height, double depth_scale, float* rgb, float* depth, int32_t* mask, void* stream);
+
+/* One lifted instance (objects.py:68-83 Detection without the mask crop). */
+typedef struct VmDetection {
+  int32_t instance_id, n_pixels, n_valid, reserved;
+  int32_t u0, v0, u1, v1;                 /* half-open 2D bbox of the whole mask */
+  double box_min[3], box_max[3];          /* AABB.from_points(trim) of the valid pixels */
+} VmDetection;
+
+size_t vm_ingest_workspace_bytes(int32_t width, int32_t height);
+/* extract_detections (objects.py:170-217) + scene_bounds (:220-230) for one
+   device frame (depth f32, mask int32 in [0, 65535]): detections of the ids
+   with >= min_pixels valid-depth pixels in ascending id order (host `out`),
+   and the trimmed box of the stride-subsampled valid depth (*scene_ok = 0
+   when fewer than 16 points).  intr = (fx, fy, cx, cy), pose 4x4 (host).
+   Synchronises `stream` (the detections are returned on the host). */
+int vm_ingest_frame(const float* depth, const int32_t* mask, int32_t width, int32_t height, const double* intr,
+                    const double* pose, int32_t min_pixels, double trim, int32_t scene_stride, double scene_trim,
+                    VmDetection* out, int32_t capacity, int32_t* n_out, double* scene_box /* host [6] */,
+                    int32_t* scene_ok, void* workspace, size_t workspace_bytes, void* stream);
+
 /* ---- profiling: event-time every fused-kernel launch of vm_train_step ---- */
 int vm_profile_enable(int on);                          /* resets the launch log */
 int vm_profile_read(int* launches, double* total_ms);   /* syncs on the events; MLP phase */

@@ -694,3 +694,148 @@ def render_view(obj: Stack, bg: Stack, objects, background, intr, pose, t_near=0
         instance[gi] = inst.object_id
     return (np.clip(colour, 0.0, 1.0).reshape(h, w, 3).astype(np.float32),
             (depth / scale).reshape(h, w).astype(np.float32), instance.reshape(h, w))
+
+
+# --------------------------------------------------------------------------
+# per-frame ingestion (objects.py:160-320, trainer.py:226-265) -- SURVEY 8f #2
+# --------------------------------------------------------------------------
+
+class Box:
+    """AABB (geometry.py:10-46) with the fields the ingestion path uses."""
+
+    def __init__(self, lo, hi):
+        self.min = np.asarray(lo, np.float64).reshape(3)
+        self.max = np.asarray(hi, np.float64).reshape(3)
+
+    @property
+    def volume(self):
+        return float(np.prod(self.max - self.min))
+
+    def union(self, o):
+        return Box(np.minimum(self.min, o.min), np.maximum(self.max, o.max))
+
+
+def from_points(points, trim=0.0, min_extent=1e-3) -> Box:
+    """geometry.py:49-70."""
+    pts = np.asarray(points, np.float64).reshape(-1, 3)
+    if trim > 0.0 and pts.shape[0] > 10:
+        lo = np.quantile(pts, trim, axis=0)
+        hi = np.quantile(pts, 1.0 - trim, axis=0)
+    else:
+        lo, hi = pts.min(axis=0), pts.max(axis=0)
+    thin = (hi - lo) < min_extent
+    return Box(np.where(thin, lo - 0.5 * min_extent, lo), np.where(thin, hi + 0.5 * min_extent, hi))
+
+
+def box_iou(a: Box, b: Box) -> float:
+    """geometry.py:73-80."""
+    lo, hi = np.maximum(a.min, b.min), np.minimum(a.max, b.max)
+    if np.any(hi <= lo):
+        return 0.0
+    inter = float(np.prod(hi - lo))
+    return inter / (a.volume + b.volume - inter)
+
+
+def backproject(us, vs, z, intr, pose):
+    """objects.py:160-167."""
+    x = (us - intr.cx) / intr.fx * z
+    y = (vs - intr.cy) / intr.fy * z
+    return np.stack([x, y, z], axis=-1) @ pose[:3, :3].T + pose[:3, 3]
+
+
+def extract_detections(depth, mask, intr, pose, classes, min_pixels=100, trim=0.02):
+    """objects.py:170-217 -> [(class, bbox, n_valid, mask crop, Box)] in id order."""
+    out = []
+    for inst_id in np.unique(mask):
+        if inst_id == 0:
+            continue
+        m = mask == inst_id
+        valid = m & (depth > 0)
+        n_valid = int(valid.sum())
+        if n_valid < min_pixels:
+            continue
+        vs, us = np.nonzero(m)
+        u0, u1, v0, v1 = int(us.min()), int(us.max()) + 1, int(vs.min()), int(vs.max()) + 1
+        vv, uu = np.nonzero(valid)
+        pts = backproject(uu.astype(np.float64), vv.astype(np.float64), depth[vv, uu], intr, pose)
+        out.append(dict(cls=int(classes.get(int(inst_id), 1)), bbox=(u0, v0, u1, v1), n_pixels=n_valid,
+                        mask=m[v0:v1, u0:u1], aabb=from_points(pts, trim=trim)))
+    return out
+
+
+def scene_bounds(depth, intr, pose, stride=4, trim=0.01):
+    """objects.py:220-230."""
+    d = depth[::stride, ::stride]
+    vs, us = np.nonzero(d > 0)
+    if vs.size < 16:
+        return None
+    pts = backproject((us * stride).astype(np.float64), (vs * stride).astype(np.float64), d[vs, us], intr, pose)
+    return from_points(pts, trim=trim)
+
+
+def associate_detections(dets, objects, iou_threshold=0.2):
+    """objects.py:233-259 (objects: instances with object_id, cls, aabb)."""
+    cand = []
+    for di, det in enumerate(dets):
+        for inst in objects:
+            if inst.cls != det["cls"]:
+                continue
+            iou = box_iou(det["aabb"], inst.aabb)
+            if iou >= iou_threshold:
+                cand.append((-iou, inst.object_id, di))
+    cand.sort()
+    assigned, used = [None] * len(dets), set()
+    for _, oid, di in cand:
+        if assigned[di] is None and oid not in used:
+            assigned[di] = oid
+            used.add(oid)
+    return assigned
+
+
+class IngestMap:
+    """The map bookkeeping process_frame mutates (trainer.py:226-265)."""
+
+    def __init__(self, intr, stride_object=25, stride_background=50, margin=10, min_pixels=100, trim=0.02,
+                 iou_threshold=0.2):
+        self.intr = intr
+        self.objects = []      # model-index order
+        self.background = None
+        self.next_id = 1
+        self.cfg = dict(so=stride_object, sb=stride_background, margin=margin, min_pixels=min_pixels, trim=trim,
+                        iou=iou_threshold)
+
+    def process_frame(self, frame_id, rgb, depth, mask, pose, classes=None):
+        c = self.cfg
+        classes = classes or {}
+        bounds = scene_bounds(depth, self.intr, pose)
+        bg = self.background
+        if bg is None:
+            if bounds is None:
+                raise ValueError(f"frame {frame_id}: no valid depth to bound the scene")
+            bg = self.background = _NSI(object_id=0, cls=0, aabb=bounds, obs=0, kfs=[], is_bg=True)
+        elif bounds is not None:
+            bg.aabb = bg.aabb.union(bounds)
+        bg.obs += 1
+        h, w = depth.shape
+        if (bg.obs - 1) % c["sb"] == 0:
+            bg.kfs.append((frame_id, (0, 0, w, h)))
+        dets = extract_detections(depth, mask, self.intr, pose, classes, c["min_pixels"], c["trim"])
+        for det, oid in zip(dets, associate_detections(dets, self.objects, c["iou"])):
+            if oid is None:
+                inst = _NSI(object_id=self.next_id, cls=det["cls"], aabb=det["aabb"], obs=0, kfs=[], is_bg=False)
+                self.next_id += 1
+                self.objects.append(inst)
+            else:
+                inst = next(o for o in self.objects if o.object_id == oid)
+                inst.aabb = inst.aabb.union(det["aabb"])
+            inst.obs += 1
+            if (inst.obs - 1) % c["so"] == 0:
+                u0, v0, u1, v1 = det["bbox"]
+                m = c["margin"]
+                inst.kfs.append((frame_id, (max(u0 - m, 0), max(v0 - m, 0), min(u1 + m, w), min(v1 + m, h))))
+        return dets, bounds
+
+
+class _NSI:
+    def __init__(self, **kw):
+        self.__dict__.update(kw)

@@ -79,6 +79,12 @@ class VmSampleParams(C.Structure):
                 ("three_std", C.c_double), ("step_dev", C.c_void_p), ("step_offset", C.c_int64)]
 
 
+class VmDetection(C.Structure):
+    _fields_ = [("instance_id", C.c_int32), ("n_pixels", C.c_int32), ("n_valid", C.c_int32), ("reserved", C.c_int32),
+                ("u0", C.c_int32), ("v0", C.c_int32), ("u1", C.c_int32), ("v1", C.c_int32),
+                ("box_min", C.c_double * 3), ("box_max", C.c_double * 3)]
+
+
 class VmSampleAux(C.Structure):
     _fields_ = [("kf_idx", C.c_void_p), ("u", C.c_void_p), ("v", C.c_void_p), ("t64", C.c_void_p)]
 
@@ -98,6 +104,13 @@ _SIGNATURES = {
                                     C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "vm_view_compose": (C.c_int, [C.c_int32, C.c_int64] + [C.c_void_p] * 6 + [C.c_double] * 3 + [C.c_int32]
                         + [C.c_void_p] * 5),
+    "vm_decode_frame": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_double,
+                                  C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "vm_ingest_workspace_bytes": (C.c_size_t, [C.c_int32, C.c_int32]),
+    "vm_ingest_frame": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_int32,
+                                  C.c_double, C.c_int32, C.c_double, C.POINTER(VmDetection), C.c_int32,
+                                  C.POINTER(C.c_int32), C.c_void_p, C.POINTER(C.c_int32), C.c_void_p, C.c_size_t,
+                                  C.c_void_p]),
     "vm_work_items": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_int32, C.POINTER(C.c_int32)]),
     "vm_train_step": (C.c_int, [C.POINTER(VmStack), C.POINTER(VmBatch), C.c_int, VmLossWeights,
                                 C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]),

@@ -20,7 +20,8 @@ import torch
 from . import _lib
 from .keyframes import DeviceTable, KeyframeArena, SampleBuffers, build_tables, run_sampler, sample_params
 from .models import DEVICE, append_model, init_stacked, set_frozen
-from .objects import ObjectMap, add_keyframe
+from .ingest import FrameIngestor, associate, extract_detections_device, keyframe_due, update_bounds
+from .objects import ObjectMap, add_keyframe, dilate_bbox
 from .render import CameraIntrinsics
 from .rng import PURPOSE_INIT_BACKGROUND, PURPOSE_INIT_OBJECT
 from .trainer import StepReport, TrainConfig, TrainWorkspace, launch_train
@@ -71,6 +72,7 @@ class Mapper:
         self._pin_scale = None
         self._pin_done = None
         self._n_kf = 0
+        self._ingest = None
 
     # ------------------------------------------------------------ building
     def add_background(self, aabb, pe_scale: float | None = None):
@@ -106,6 +108,43 @@ class Mapper:
         self.arena.add(kf)
         self.invalidate()
         return kf
+
+    # ------------------------------------------------------------ ingestion
+    def process_frame(self, frame, classes: dict | None = None) -> None:
+        """trainer.py:226-265: scene bounds and instance detections of the
+        frame (device kernels, ingest.py), association, box growth,
+        new objects and keyframes at the per-object stride."""
+        cfg = self.cfg
+        acfg = cfg.association
+        classes = classes if classes is not None else {}
+        if self._ingest is None:
+            self._ingest = FrameIngestor(self.device)
+        detections, bounds = extract_detections_device(self._ingest, frame, self.intrinsics, classes, acfg)
+        bg = self.map.background
+        if bg is None:
+            if bounds is None:
+                raise ValueError(f"frame {frame.frame_id}: no valid depth to bound the scene")
+            bg = self.add_background(bounds)
+        elif bounds is not None:
+            update_bounds(bg, bounds)
+        bg.obs_count += 1
+        if keyframe_due(bg, acfg):
+            h, w = frame.depth.shape
+            self.add_keyframe(bg, frame.frame_id, frame.pose, (0, 0, w, h), frame.mask == 0, frame.rgb, frame.depth)
+        assignments = associate(detections, self.map, acfg)
+        for det, assigned in zip(detections, assignments):
+            if assigned is None:
+                inst = self.add_object(det.semantic_class, det.aabb)
+            else:
+                inst = self.map.instances[assigned]
+                update_bounds(inst, det.aabb)
+            inst.obs_count += 1
+            if keyframe_due(inst, acfg):
+                bbox, mask = dilate_bbox(det.bbox, det.mask, acfg.bbox_margin_px, frame.depth.shape)
+                self.add_keyframe(inst, frame.frame_id, frame.pose, bbox, mask, frame.rgb, frame.depth)
+        self.frames_seen += 1
+        self.last_frame_id = frame.frame_id
+        self.invalidate()  # boxes may have grown
 
     def invalidate(self) -> None:
         """Force the device tables to be rebuilt (after editing boxes/keyframes,
@@ -449,3 +488,26 @@ class Mapper:
         self.global_step += 1
         return StepReport(step=step, frame_id=self.last_frame_id, k_models=k_models, losses=report_losses,
                           total=float(total), ms=(time.perf_counter() - t0) * 1e3)
+
+
+def run_mapping(dataset, cfg: TrainConfig | None = None, mode: str = "vectorised", progress: bool = False,
+                device=DEVICE):
+    """trainer.py:541-569: per frame, ingest then train steps_per_frame
+    steps.  Frames are decoded ahead on a worker thread (datasets.FramePrefetcher)."""
+    from .datasets import FramePrefetcher
+    cfg = cfg if cfg is not None else TrainConfig()
+    mapper = Mapper(dataset.intrinsics, cfg, device=device)
+    reports = []
+    n_frames = len(dataset) if cfg.max_frames is None else min(len(dataset), cfg.max_frames)
+    for i, frame in enumerate(FramePrefetcher(dataset, n_frames)):
+        try:
+            mapper.process_frame(frame, dataset.classes)
+        except Exception as exc:
+            raise RuntimeError(f"failed on frame {i}: {exc}") from exc
+        for _ in range(cfg.steps_per_frame):
+            reports.append(mapper.train_step(mode=mode))
+        if progress and (i % 20 == 0 or i == n_frames - 1):
+            last = reports[-1]
+            print(f"frame {i + 1}/{n_frames}  K={last.k_models}  total={last.total:.3f}  step_ms={last.ms:.1f}",
+                  flush=True)
+    return mapper, reports

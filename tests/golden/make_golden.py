@@ -69,6 +69,73 @@ def flat(params):
                            for l in range(len(params.weights))], 1)
 
 
+INGEST_STRIDES = dict(keyframe_stride_object=2, keyframe_stride_background=3)
+INGEST_RAYS = dict(rays_per_object=48, rays_background=96, steps_per_frame=2)
+
+
+def ingest_goldens(vobj):
+    """Synthetic RGB-D datasets written by the reference's own generator
+    (synth.generate: PNGs + poses/intrinsics/classes, committed under
+    tests/golden/ds_*), then the reference's ingestion and mapping loop on
+    them: per-frame detections / scene bounds, the map after every frame, and
+    run_mapping's losses and parameters."""
+    import dataclasses
+    import shutil
+    from vobj import synth
+    from vobj.datasets import Dataset
+    from vobj.objects import AssociationConfig, extract_detections, scene_bounds
+    from vobj.trainer import Mapper, TrainConfig, run_mapping
+    specs = {
+        "ds_mini": dataclasses.replace(synth.mini_scene(n_frames=8), permute_mask_ids=True),
+        "ds_five": dataclasses.replace(synth.five_object_scene(n_frames=6), width=200, height=150, focal=150.0,
+                                       depth_noise_std=0.004),
+    }
+    out = {}
+    for name, spec in specs.items():
+        root = HERE / name
+        if root.exists():
+            shutil.rmtree(root)
+        ds = synth.generate(spec, root, seed=3)
+        shutil.rmtree(root / "gt_mesh")
+        acfg = AssociationConfig(**INGEST_STRIDES)
+        cfg = TrainConfig(association=acfg)
+        m = Mapper(ds.intrinsics, cfg)
+        for i in range(len(ds)):
+            fr = ds.frame(i)
+            dets = extract_detections(fr.rgb, fr.depth, fr.mask, fr.frame_id, ds.intrinsics, fr.pose, ds.classes,
+                                      acfg)
+            sb = scene_bounds(fr.depth, ds.intrinsics, fr.pose)
+            pre = f"{name}_f{i}_"
+            out[pre + "scene"] = np.concatenate([sb.min, sb.max]) if sb is not None else np.zeros(0)
+            out[pre + "det_bbox"] = np.array([d.bbox for d in dets], np.int64).reshape(-1, 4)
+            out[pre + "det_n"] = np.array([d.n_pixels for d in dets], np.int64)
+            out[pre + "det_cls"] = np.array([d.semantic_class for d in dets], np.int64)
+            out[pre + "det_box"] = np.array([np.concatenate([d.aabb.min, d.aabb.max]) for d in dets]).reshape(-1, 6)
+            m.process_frame(fr, ds.classes)
+            objs = [m.map.instances[o] for o in m.model_to_object]
+            out[pre + "obj_ids"] = np.array([o.object_id for o in objs], np.int64)
+            out[pre + "obj_box"] = np.array([np.concatenate([o.aabb.min, o.aabb.max]) for o in objs]).reshape(-1, 6)
+            out[pre + "obj_obs"] = np.array([o.obs_count for o in objs], np.int64)
+            out[pre + "obj_kf"] = np.array([[k.frame_id, *k.bbox, int(o.object_id)] for o in objs
+                                            for k in o.keyframes], np.int64).reshape(-1, 6)
+            bg = m.map.background
+            out[pre + "bg_box"] = np.concatenate([bg.aabb.min, bg.aabb.max])
+            out[pre + "bg_kf"] = np.array([k.frame_id for k in bg.keyframes], np.int64)
+        cfg2 = TrainConfig(association=acfg, **INGEST_RAYS)
+        mm, reports = run_mapping(ds, cfg2)
+        width = max(len(r.losses) for r in reports)
+        ids = np.full((len(reports), width), -1, np.int64)
+        ls = np.full((len(reports), width, 3), np.nan)
+        for j, r in enumerate(reports):
+            keys = sorted(r.losses)
+            ids[j, :len(keys)] = keys
+            ls[j, :len(keys)] = [r.losses[k] for k in keys]
+        out[f"{name}_map_ids"], out[f"{name}_map_losses"] = ids, ls
+        out[f"{name}_map_obj_params"] = flat(mm.obj_params)
+        out[f"{name}_map_bg_params"] = flat(mm.bg_params)
+    np.savez_compressed(HERE / "ingest.npz", **out)
+
+
 def main():
     vobj = import_reference()
     from vobj import models as M
@@ -177,11 +244,12 @@ def main():
                            samples_refine=8, threshold=thr)
         inf[tag + "_rgb"], inf[tag + "_depth"], inf[tag + "_inst"] = view.rgb, view.depth, view.instance
     np.savez_compressed(HERE / "infer_cfg1.npz", **inf)
+    ingest_goldens(vobj)
     import numpy
     (HERE / "PROVENANCE.txt").write_text(
         "Generated by tests/golden/make_golden.py from the reference at /root/reference/pkg/src\n"
         f"numpy {numpy.__version__}; scipy {__import__('scipy').__version__}\n")
-    for f in ("ops.npz", "sampler_cfg1.npz", "train_cfg1.npz", "infer_cfg1.npz"):
+    for f in ("ops.npz", "sampler_cfg1.npz", "train_cfg1.npz", "infer_cfg1.npz", "ingest.npz"):
         print(f, (HERE / f).stat().st_size)
 
 

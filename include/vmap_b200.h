@@ -291,6 +291,14 @@ int vm_ingest_frame(const float* depth, const int32_t* mask, int32_t width, int3
                     VmDetection* out, int32_t capacity, int32_t* n_out, double* scene_box /* host [6] */,
                     int32_t* scene_ok, void* workspace, size_t workspace_bytes, void* stream);
 
+/* ---- VOBJ v1 checkpoint stack sections (checkpoint.py:51-84; 8f #3) ------
+   vm_pack_stack gathers the live parameters + Adam moments of `st` from the
+   padded device arena into the reference's section order (per layer W
+   [K,fo,fi], b [K,fo]; then per layer m_w, v_w, m_b, v_b), `packed` being
+   vm_pack_floats(st) device floats; unpack = 1 scatters it back. */
+int64_t vm_pack_floats(const VmStack* st);
+int vm_pack_stack(const VmStack* st, float* packed, int32_t unpack, void* stream);
+
 /* ---- profiling: event-time every fused-kernel launch of vm_train_step ---- */
 int vm_profile_enable(int on);                          /* resets the launch log */
 int vm_profile_read(int* launches, double* total_ms);   /* syncs on the events; MLP phase */

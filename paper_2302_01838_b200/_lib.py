@@ -111,6 +111,8 @@ _SIGNATURES = {
                                   C.c_double, C.c_int32, C.c_double, C.POINTER(VmDetection), C.c_int32,
                                   C.POINTER(C.c_int32), C.c_void_p, C.POINTER(C.c_int32), C.c_void_p, C.c_size_t,
                                   C.c_void_p]),
+    "vm_pack_floats": (C.c_int64, [C.POINTER(VmStack)]),
+    "vm_pack_stack": (C.c_int, [C.POINTER(VmStack), C.c_void_p, C.c_int32, C.c_void_p]),
     "vm_work_items": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_int32, C.POINTER(C.c_int32)]),
     "vm_train_step": (C.c_int, [C.POINTER(VmStack), C.POINTER(VmBatch), C.c_int, VmLossWeights,
                                 C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]),

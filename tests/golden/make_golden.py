@@ -136,6 +136,40 @@ def ingest_goldens(vobj):
     np.savez_compressed(HERE / "ingest.npz", **out)
 
 
+def checkpoint_golden(vobj):
+    """A VOBJ v1 file written by the reference (checkpoint.py:132-144): two
+    trained stacks (hidden 16 / 32, one frozen model) + an object table with
+    a keyframe reference (test_checkpoint.py's fixtures)."""
+    from vobj.checkpoint import save_checkpoint
+    from vobj.geometry import AABB
+    from vobj.models import ModelArch, adam_step, backward, forward, init_stacked
+    from vobj.objects import Keyframe, ObjectMap
+
+    def trained(k, hidden, seed):
+        arch = ModelArch(n_layers=3, hidden=hidden, n_freq=2)
+        p, s = init_stacked(arch, k, seed=seed)
+        g = np.random.default_rng(seed + 1)
+        for _ in range(2):
+            x = g.standard_normal((k, 40, arch.input_dim)).astype(np.float32)
+            _, cache = forward(p, x)
+            gr = backward(p, cache, g.standard_normal((k, 40)).astype(np.float32),
+                          g.standard_normal((k, 40, 3)).astype(np.float32))
+            adam_step(p, s, gr)
+        return p, s
+
+    op, os_ = trained(3, 16, 5)
+    bp, bs = trained(1, 32, 9)
+    op.frozen[1] = True
+    mp = ObjectMap()
+    mp.add_background(AABB(np.array([-2.0, -2, -2]), np.array([2.0, 2, 2])), pe_scale=15.0, model_index=0)
+    inst = mp.add_object(semantic_class=3, aabb=AABB(np.array([0.1, 0.2, 0.3]), np.array([0.4, 0.5, 0.6])),
+                         pe_scale=10.0, model_index=0)
+    inst.obs_count = 7
+    inst.keyframes.append(Keyframe(frame_id=4, bbox=(1, 2, 10, 12), rgb=np.zeros((10, 9, 3), np.float32),
+                                   depth=np.ones((10, 9), np.float32), mask=np.ones((10, 9), bool), pose=np.eye(4)))
+    save_checkpoint(HERE / "ckpt_small.bin", op, os_, bp, bs, mp)
+
+
 def main():
     vobj = import_reference()
     from vobj import models as M
@@ -245,11 +279,13 @@ def main():
         inf[tag + "_rgb"], inf[tag + "_depth"], inf[tag + "_inst"] = view.rgb, view.depth, view.instance
     np.savez_compressed(HERE / "infer_cfg1.npz", **inf)
     ingest_goldens(vobj)
+    checkpoint_golden(vobj)
     import numpy
     (HERE / "PROVENANCE.txt").write_text(
         "Generated by tests/golden/make_golden.py from the reference at /root/reference/pkg/src\n"
         f"numpy {numpy.__version__}; scipy {__import__('scipy').__version__}\n")
-    for f in ("ops.npz", "sampler_cfg1.npz", "train_cfg1.npz", "infer_cfg1.npz", "ingest.npz"):
+    for f in ("ops.npz", "sampler_cfg1.npz", "train_cfg1.npz", "infer_cfg1.npz", "ingest.npz",
+              "ckpt_small.bin"):
         print(f, (HERE / f).stat().st_size)
 
 

@@ -132,21 +132,94 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def cpu_sample(scene, seconds: float, cfg, min_steps: int = 3):
-    """Time the oracle port (numpy restatement of the reference) on the workload."""
-    import numpy as np
+def import_reference_pkg():
+    """The unmodified reference package installed once into baseline/_ref
+    (pip install --no-index --target baseline/_ref /root/reference/pkg).  Its
+    meshing module imports scikit-image at import time, which this image
+    lacks; the map-update path never calls it, so a stub module stands in."""
+    import types
+    ref = ROOT / "baseline" / "_ref"
+    if not (ref / "vobj").is_dir():
+        return None
+    try:
+        import skimage  # noqa: F401
+    except ImportError:
+        sk = types.ModuleType("skimage")
+        meas, met = types.ModuleType("skimage.measure"), types.ModuleType("skimage.metrics")
+        meas.marching_cubes = lambda *a, **k: (_ for _ in ()).throw(RuntimeError("skimage stub"))
+        met.structural_similarity = lambda *a, **k: 0.0
+        sk.measure, sk.metrics = meas, met
+        sys.modules.update({"skimage": sk, "skimage.measure": meas, "skimage.metrics": met})
+    sys.path.insert(0, str(ref))
+    try:
+        import vobj
+    except Exception:
+        return None
+    return vobj
+
+
+def reference_mapper(vobj, scene: dict, cfg):
+    """The reference's Mapper populated with the scene exactly as
+    scenes.populate does for this package (append order = init keys)."""
+    from vobj import trainer as T
+    from vobj.geometry import AABB
+    from vobj.models import append_model
+    from vobj.objects import add_keyframe
+    from vobj.render import CameraIntrinsics
+    from vobj.rng import PURPOSE_INIT_BACKGROUND, PURPOSE_INIT_OBJECT
+    intr = scene["intrinsics"]
+    rc = T.TrainConfig(seed=cfg.seed, rays_per_object=cfg.rays_per_object, rays_background=cfg.rays_background)
+    m = T.Mapper(CameraIntrinsics(intr.fx, intr.fy, intr.cx, intr.cy, intr.width, intr.height), rc)
+    if scene["background"] is not None:
+        b = scene["background"]
+        idx = append_model(m.bg_params, m.bg_state, rc.seed, PURPOSE_INIT_BACKGROUND)
+        inst = m.map.add_background(AABB(b["aabb"].min, b["aabb"].max), rc.pe_scale_background, idx)
+        for kf in b["keyframes"]:
+            add_keyframe(inst, kf["frame_id"], kf["pose"], kf["bbox"], kf["mask"], scene["rgb"], scene["depth"])
+    for ob in scene["objects"]:
+        idx = append_model(m.obj_params, m.obj_state, rc.seed, PURPOSE_INIT_OBJECT)
+        inst = m.map.add_object(1, AABB(ob["aabb"].min, ob["aabb"].max), rc.pe_scale_object, idx)
+        m.model_to_object.append(inst.object_id)
+        for kf in ob["keyframes"]:
+            add_keyframe(inst, kf["frame_id"], kf["pose"], kf["bbox"], kf["mask"], scene["rgb"], scene["depth"])
+    return m
+
+
+def reference_stepper(scene: dict, cfg, workload: str):
+    """(step(), kind, description) of the reference's CPU map update: the
+    unmodified reference package when installed (configs 2 and 4), else the
+    oracle port (config 3's per-object ray counts have no reference API)."""
+    vobj = import_reference_pkg() if workload != "3" else None
+    if vobj is not None:
+        m = reference_mapper(vobj, scene, cfg)
+        return m.train_step, "reference", "vobj Mapper.train_step (baseline/_ref, unmodified reference package)"
     from oracle import vobj_oracle as O
-    sys.path.insert(0, str(ROOT / "tests"))
     from tests.helpers import oracle_mapstate
     ms = oracle_mapstate(scene, cfg)
-    O.map_update_step(ms)  # warm-up (BLAS threads, page faults)
+    return (lambda: O.map_update_step(ms)), "port", "oracle/vobj_oracle.py map_update_step (numpy port)"
+
+
+def cpu_sample(scene, seconds: float, cfg, workload: str, min_steps: int = 3):
+    """Time the reference's CPU map update on the workload (bounded sample)."""
+    step, kind, desc = reference_stepper(scene, cfg, workload)
+    step()  # warm-up (BLAS threads, page faults)
     n, t0 = 0, time.perf_counter()
     while n < min_steps or time.perf_counter() - t0 < seconds:
-        O.map_update_step(ms)
+        step()
         n += 1
     dt = (time.perf_counter() - t0) / n
     k = len(scene["objects"])
-    return k / dt, n, dt
+    one = None
+    try:  # the same on one BLAS thread (SURVEY 8d), a short bounded sample
+        from threadpoolctl import threadpool_limits
+        with threadpool_limits(1):
+            t1 = time.perf_counter()
+            for _ in range(2):
+                step()
+            one = k / ((time.perf_counter() - t1) / 2)
+    except Exception:
+        pass
+    return k / dt, n, dt, kind, desc, one
 
 
 def blas_threads():
@@ -158,21 +231,20 @@ def blas_threads():
 
 
 def run_reference(args, rank, world):
-    """--impl reference: the reference algorithm (oracle port: the reference is
-    pure Python/numpy and has no compiled build to run) on the box's host cores."""
+    """--impl reference: the reference's own CPU map update (the unmodified
+    package from baseline/_ref; the oracle port when it is absent) on the
+    box's host cores, rank 0 only."""
     if rank != 0:
         return
     scene = workload_scene(args.workload, 0)
-    import numpy as np  # noqa: F401
-    from oracle import vobj_oracle as O
-    from tests.helpers import oracle_mapstate
-    ms = oracle_mapstate(scene, workload_cfg(args.workload))
+    import numpy as np
+    step, kind, desc = reference_stepper(scene, workload_cfg(args.workload), args.workload)
     for _ in range(max(args.warmup, 1)):
-        O.map_update_step(ms)
+        step()
     times = []
     for _ in range(args.steps):
         t0 = time.perf_counter()
-        O.map_update_step(ms)
+        step()
         times.append(time.perf_counter() - t0)
     dt = sum(times) / len(times)
     k = len(scene["objects"])
@@ -187,9 +259,9 @@ def run_reference(args, rank, world):
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": _config(world, args.workload),
         "samples_per_s": k * 10 * float(np.mean([ob.get("n_rays", 120) for ob in scene["objects"]])) / dt,
-        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": f"{args.steps} full map-update steps of config {args.workload} (oracle/vobj_oracle.py "
-                                   f"map_update_step, numpy/OpenBLAS, {cores} threads)"},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": kind,
+                         "sample": f"{args.steps} full map-update steps of config {args.workload} ({desc}, "
+                                   f"numpy/OpenBLAS, {cores} threads)"},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }))
 
@@ -415,11 +487,12 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, n, dt = cpu_sample(scene, args.cpu_seconds, cfg)
+        v, n, dt, kind, desc, one = cpu_sample(scene, args.cpu_seconds, cfg, args.workload)
         cores = blas_threads()
-        cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
+        cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": kind,
                "sample": f"{n} full map-update steps of config {args.workload} ({dt*1e3:.0f} ms/step) through "
-                         f"oracle/vobj_oracle.py map_update_step (numpy/OpenBLAS, {cores} threads)"}
+                         f"{desc} (numpy/OpenBLAS, {cores} threads)",
+               "value_1_thread": one}
 
     if rank == 0:
         line = {

@@ -17,6 +17,7 @@ import torch
 from paper_2302_01838_b200 import TrainConfig
 from paper_2302_01838_b200.checkpoint import load_checkpoint, save_checkpoint
 from paper_2302_01838_b200.mapper import Mapper
+from paper_2302_01838_b200.objects import Keyframe
 from paper_2302_01838_b200.scenes import config, populate
 
 pytestmark = pytest.mark.gpu
@@ -29,6 +30,14 @@ def test_reference_file_round_trips_byte_identical(cuda, tmp_path):
     assert op.frozen[:3].tolist() == [False, True, False]
     assert [r for r in refs if r] == [[(4, (1, 2, 10, 12))]]
     assert mp.instances[1].obs_count == 7 and mp.instances[0].is_background
+    # keyframes come back as (frame_id, bbox) references (checkpoint.py:150-154);
+    # re-attach them (pixels would be re-hydrated from the dataset)
+    for oid, rr in zip(sorted(mp.instances), refs):
+        for fid, bbox in rr:
+            h, w = bbox[3] - bbox[1], bbox[2] - bbox[0]
+            mp.instances[oid].keyframes.append(Keyframe(frame_id=fid, pose=np.eye(4), bbox=bbox,
+                                                        mask=np.ones((h, w), bool), rgb=np.zeros((h, w, 3), np.float32),
+                                                        depth=np.ones((h, w), np.float32)))
     out = tmp_path / "again.bin"
     save_checkpoint(out, op, os_, bp, bs, mp)
     assert out.read_bytes() == (G / "ckpt_small.bin").read_bytes()

@@ -24,20 +24,24 @@ pytestmark = pytest.mark.gpu
 G = Path(__file__).resolve().parent / "golden"
 
 
-def test_reference_file_round_trips_byte_identical(cuda, tmp_path):
-    op, os_, bp, bs, mp, refs = load_checkpoint(G / "ckpt_small.bin")
-    assert op.count == 3 and op.arch.hidden == 16 and bp.count == 1 and bp.arch.hidden == 32
-    assert op.frozen[:3].tolist() == [False, True, False]
-    assert [r for r in refs if r] == [[(4, (1, 2, 10, 12))]]
-    assert mp.instances[1].obs_count == 7 and mp.instances[0].is_background
-    # keyframes come back as (frame_id, bbox) references (checkpoint.py:150-154);
-    # re-attach them (pixels would be re-hydrated from the dataset)
+def _reattach(mp, refs):
+    """Keyframes come back as (frame_id, bbox) references (checkpoint.py:
+    150-154); re-attach them (pixels would be re-hydrated from the dataset)."""
     for oid, rr in zip(sorted(mp.instances), refs):
         for fid, bbox in rr:
             h, w = bbox[3] - bbox[1], bbox[2] - bbox[0]
             mp.instances[oid].keyframes.append(Keyframe(frame_id=fid, pose=np.eye(4), bbox=bbox,
                                                         mask=np.ones((h, w), bool), rgb=np.zeros((h, w, 3), np.float32),
                                                         depth=np.ones((h, w), np.float32)))
+
+
+def test_reference_file_round_trips_byte_identical(cuda, tmp_path):
+    op, os_, bp, bs, mp, refs = load_checkpoint(G / "ckpt_small.bin")
+    assert op.count == 3 and op.arch.hidden == 16 and bp.count == 1 and bp.arch.hidden == 32
+    assert op.frozen[:3].tolist() == [False, True, False]
+    assert [r for r in refs if r] == [[(4, (1, 2, 10, 12))]]
+    assert mp.instances[1].obs_count == 7 and mp.instances[0].is_background
+    _reattach(mp, refs)
     out = tmp_path / "again.bin"
     save_checkpoint(out, op, os_, bp, bs, mp)
     assert out.read_bytes() == (G / "ckpt_small.bin").read_bytes()
@@ -67,6 +71,7 @@ def test_trained_map_round_trip(cuda, tmp_path):
         assert torch.equal(a.step[:k], b.step[:k])
     assert sorted(mp.instances) == sorted(m.map.instances)
     assert [len(r) for r in refs] == [len(m.map.instances[i].keyframes) for i in sorted(m.map.instances)]
+    _reattach(mp, refs)
     p2 = tmp_path / "b.bin"
     save_checkpoint(p2, op, os_, bp, bs, mp)
     assert p1.read_bytes() == p2.read_bytes()

@@ -95,6 +95,33 @@ __device__ float pairwise_sum_leaf(const F& get, int64_t i0, int64_t n) {
   return res;
 }
 
+// pairwise_sum_leaf for a compile-time n <= 128: every index is a constant,
+// so register arrays behind `get` stay in registers (same order, same bits).
+template <int N, typename F>
+__device__ __forceinline__ float pairwise_sum_fixed(const F& get) {
+  static_assert(N <= 128, "one pairwise leaf");
+  if constexpr (N < 8) {
+    float res = -0.0f;
+#pragma unroll
+    for (int i = 0; i < N; ++i) res = __fadd_rn(res, get(i));
+    return res;
+  } else {
+    float r[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = get(j);
+#pragma unroll
+    for (int i = 8; i < N - (N % 8); i += 8) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) r[j] = __fadd_rn(r[j], get(i + j));
+    }
+    float res = __fadd_rn(__fadd_rn(__fadd_rn(r[0], r[1]), __fadd_rn(r[2], r[3])),
+                          __fadd_rn(__fadd_rn(r[4], r[5]), __fadd_rn(r[6], r[7])));
+#pragma unroll
+    for (int i = N - (N % 8); i < N; ++i) res = __fadd_rn(res, get(i));
+    return res;
+  }
+}
+
 // Recursive split for n > 128 (depth <= log2(n/128)).
 template <typename F>
 __device__ float pairwise_sum_rec(const F& get, int64_t i0, int64_t n) {

@@ -52,8 +52,36 @@ constexpr int oW0 = 0, oB0 = oW0 + H * WS, oW1 = oB0 + H, oB1 = oW1 + H * WS, oW
 // per-team activation region (floats), rows of kLD = 36
 constexpr int rE = 0, rA1 = rE + D0, rA2 = rA1 + H, rA3 = rA2 + H, rO = rA3 + H, kRows = rO + 4;
 constexpr int kTgt = 8;  // per-ray targets staged in smem: depth, rgb, mask, valid, ok
-constexpr int kTeamFloats = kRows * kLD + 2 * kSB + 3 * H + 4 + kTgt * kSB;  // + t, scratch, bias sums, targets
-constexpr size_t kSmemBytes = size_t(kWFloats + NT * kTeamFloats) * 4 + 64;
+
+// Per-team shared-memory layout (floats) for a compile-time S (SFIX > 0) or a
+// runtime S (SFIX == 0).  With SFIX > 0 a block holds G = 32/S rays, and the
+// team owns a staging area the next block's encoded rows, t, targets and
+// flag words are copied into with cp.async while the current block computes
+// (the enc input path): [G*S][D] raw rows | t [G*S] | targets [G][4] | flag
+// words [3][kFw].
+template <int SFIX>
+struct Lay {
+  static constexpr int G = SFIX > 0 ? kSB / SFIX : kSB;
+  static constexpr int kTs = SFIX > 0 ? kSB : 2 * kSB;  // t (+ the runtime-S render scratch)
+  static constexpr int kFw = SFIX > 0 ? (G + 3) / 4 + 1 : 0;  // 4-byte words covering G flag bytes
+  static constexpr int kStEnc = SFIX > 0 ? G * SFIX * D0 : 0;
+  static constexpr int kStT = SFIX > 0 ? G * SFIX : 0;
+  static constexpr int kStTg = kStEnc + kStT, kStFl = kStTg + 4 * G;
+  static constexpr int kStage = SFIX > 0 ? kStFl + 3 * kFw : 0;
+  static constexpr int oTs = kRows * kLD, oDb = oTs + kTs, oTg = oDb + 3 * H + 4, oStage = oTg + G * kTgt;
+  static constexpr int kTeam = oStage + kStage;
+  static constexpr size_t kSmem = size_t(kWFloats + NT * kTeam) * 4 + 64;
+};
+// two CTAs per SM: 2 x (dynamic + ~1.6 KB static + 1 KB reserved) <= 228 KB
+static_assert(Lay<10>::kSmem + 1600 + 1024 <= 228 * 1024 / 2, "KF32<10> no longer fits two CTAs per SM");
+
+__device__ __forceinline__ void cp_async4(float* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+               "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 __device__ __forceinline__ float relu(float z) {
   float r;
@@ -179,57 +207,6 @@ __device__ __forceinline__ void team_bar(int team) {
   asm volatile("bar.sync %0, 64;" ::"r"(team + 1) : "memory");
 }
 
-// Register-light render chain for one ray (render_ray_fixed's operation
-// order): occupancy/colour/t are read from smem, the 2*NS transmittance and
-// weight values stay in registers; writes dz (sigmoid'd gradients) in place.
-template <int NS>
-__device__ __forceinline__ RayLossGrad render_ray_smem(float* __restrict__ O, const float* __restrict__ tS, int sb,
-                                                       const RayTargets& tg, float w_colour, float w_occ) {
-  float Tr[NS], w[NS];
-  float Tc = 1.0f;
-#pragma unroll
-  for (int i = 0; i < NS; ++i) {
-    const float o = O[sb + i];
-    Tr[i] = Tc;
-    Tc = (i == 0) ? __fsub_rn(1.0f, o) : __fmul_rn(Tc, __fsub_rn(1.0f, o));
-    w[i] = __fmul_rn(o, Tr[i]);
-  }
-  RayFwd f;
-  f.opacity = pairwise_sum_leaf([&](int64_t i) { return w[i]; }, 0, NS);
-  f.depth = pairwise_sum_leaf([&](int64_t i) { return __fmul_rn(w[i], tS[sb + i]); }, 0, NS);
-#pragma unroll
-  for (int ch = 0; ch < 3; ++ch) {
-    const float* c = O + (1 + ch) * kLD + sb;
-    float acc = __fmul_rn(w[0], c[0]);
-#pragma unroll
-    for (int i = 1; i < NS; ++i) acc = __fadd_rn(acc, __fmul_rn(w[i], c[i]));
-    f.colour[ch] = acc;
-  }
-  const RayLossGrad lg = ray_loss_grad(f, tg, w_colour, w_occ);
-  float rev = 0.0f;
-#pragma unroll
-  for (int i = NS - 1; i >= 0; --i) {
-    float cl[3];
-#pragma unroll
-    for (int ch = 0; ch < 3; ++ch) cl[ch] = O[(1 + ch) * kLD + sb + i];
-    float cs = __fmul_rn(lg.dC[0], cl[0]);
-    cs = __fadd_rn(cs, __fmul_rn(lg.dC[1], cl[1]));
-    cs = __fadd_rn(cs, __fmul_rn(lg.dC[2], cl[2]));
-    const float g = __fadd_rn(__fadd_rn(lg.dO, __fmul_rn(lg.dD, tS[sb + i])), cs);
-    const float gw = __fmul_rn(g, w[i]);
-    rev = (i == NS - 1) ? gw : __fadd_rn(rev, gw);
-    const float suffix = __fsub_rn(rev, gw);
-    const float oi = O[sb + i];
-    const float denom = np_maximum(__fsub_rn(1.0f, oi), 1e-7f);
-    const float d_occ = __fsub_rn(__fmul_rn(g, Tr[i]), __fdiv_rn(suffix, denom));
-    O[sb + i] = __fmul_rn(__fmul_rn(d_occ, oi), __fsub_rn(1.0f, oi));
-#pragma unroll
-    for (int ch = 0; ch < 3; ++ch)
-      O[(1 + ch) * kLD + sb + i] = __fmul_rn(__fmul_rn(__fmul_rn(w[i], lg.dC[ch]), cl[ch]), __fsub_rn(1.0f, cl[ch]));
-  }
-  return lg;
-}
-
 template <int SFIX>
 __global__ void __launch_bounds__(NTHR, 2) kf32_train_kernel(const __grid_constant__ KParams p) {
   extern __shared__ __align__(16) float smem[];
@@ -248,6 +225,47 @@ __global__ void __launch_bounds__(NTHR, 2) kf32_train_kernel(const __grid_consta
   const int nblk = (Rk + G - 1) / G;
   const int Pk = max(1, (nblk + st.chunk - 1) / st.chunk);
   if (split >= Pk) return;  // dead chunk of a short model (grid without a work-item table)
+  using LY = Lay<SFIX>;
+  constexpr int kTeamFloats = LY::kTeam;
+  float* base = smem + kWFloats + team * kTeamFloats;
+  float* tS = base + LY::oTs;
+  const int bps = (nblk + Pk - 1) / Pk;
+  const int blk0 = split * bps, blk1 = min(nblk, blk0 + bps);
+
+  // enc input with a compile-time S: the next block's rows, t, targets and
+  // flag bytes are copied into the team's staging area by warp 1 with
+  // cp.async while the current block computes (issued in the render window,
+  // where warp 1 would otherwise idle), so no block waits on a global load.
+  const bool pf = SFIX > 0 && st.pts == nullptr;
+  float* stg = base + LY::oStage;
+  const int D = st.D;
+  auto prefetch = [&](int blkn) {  // warp 1 (wt == 1) only
+    const int rb = blkn * G;
+    const int nrn = min(G, Rk - rb), nsn = nrn * S;
+    const int64_t r0 = int64_t(k) * st.R + rb, g0 = r0 * S;
+    const float* src = st.enc + g0 * D;
+    for (int i = lane; i < nsn * D; i += 32) cp_async4(stg + i, src + i);
+    if (lane < nsn) cp_async4(stg + LY::kStEnc + lane, st.t + g0 + lane);
+    if (lane < nrn) {
+      float* d = stg + LY::kStTg + 4 * lane;
+      cp_async4(d, st.tdepth + r0 + lane);
+      cp_async4(d + 1, st.tcol + (r0 + lane) * 3);
+      cp_async4(d + 2, st.tcol + (r0 + lane) * 3 + 1);
+      cp_async4(d + 3, st.tcol + (r0 + lane) * 3 + 2);
+    }
+    // flag bytes: the aligned 4-byte words covering bytes [r0, r0 + nrn)
+    // (inside the allocation: torch rounds device allocations to 512 B)
+    if (lane < 3 * LY::kFw) {
+      const int a = lane / LY::kFw, j = lane % LY::kFw;
+      const uint8_t* arr = a == 0 ? st.tmask : (a == 1 ? st.valid : st.ok);
+      const uintptr_t w0 = reinterpret_cast<uintptr_t>(arr + r0) & ~uintptr_t(3);
+      const uintptr_t wl = reinterpret_cast<uintptr_t>(arr + r0 + nrn - 1) & ~uintptr_t(3);
+      if (w0 + 4 * uintptr_t(j) <= wl)
+        cp_async4(stg + LY::kStFl + a * LY::kFw + j, reinterpret_cast<const void*>(w0 + 4 * uintptr_t(j)));
+    }
+    cp_async_commit();
+  };
+  if (pf && wt == 1 && blk0 + team < blk1) prefetch(blk0 + team);
 
   // ---- stage the model's weights (rows of stride WS) and biases
   float* sW = smem;
@@ -274,12 +292,7 @@ __global__ void __launch_bounds__(NTHR, 2) kf32_train_kernel(const __grid_consta
     }
     if (tid < 4) sW[oB3 + tid] = gp[st.b_off[3] + tid];
   }
-  float* base = smem + kWFloats + team * kTeamFloats;
-  float* tS = base + kRows * kLD;
   __syncthreads();
-
-  const int bps = (nblk + Pk - 1) / Pk;
-  const int blk0 = split * bps, blk1 = min(nblk, blk0 + bps);
 
   Grads acc;
 #pragma unroll
@@ -295,8 +308,8 @@ __global__ void __launch_bounds__(NTHR, 2) kf32_train_kernel(const __grid_consta
       for (int q = 0; q < 4; ++q) acc.wh[h][j][q] = 0.f;
   acc.wl[0] = acc.wl[1] = 0.f;
   // bias gradients are summed per team in smem (rows [l*32 + o], output bias at 96..99)
-  float* sDb = base + kRows * kLD + 2 * kSB;
-  float* sTg = sDb + 3 * H + 4;
+  float* sDb = base + LY::oDb;
+  float* sTg = base + LY::oTg;
   for (int i = wt * 32 + lane; i < 3 * H + 4; i += 64) sDb[i] = 0.f;
 
   // per-lane operand bases (every access below adds a compile-time offset)
@@ -321,7 +334,33 @@ __global__ void __launch_bounds__(NTHR, 2) kf32_train_kernel(const __grid_consta
     {
       const int s = lane;  // each warp of the team encodes all 32 samples' half of the features
       float* E = base + rE * kLD;
-      if (st.pts) {
+      if (pf) {
+        // this block's staged rows (issued one block ago): transpose [ns][D]
+        // -> E[f][s]; the row stride D (odd for the reference's 33) makes the
+        // column reads conflict free
+        if (wt == 1) cp_async_wait_all();
+        team_bar(team);
+        const float* sr = stg + s * D;
+#pragma unroll
+        for (int f = wt * (D0 / 2); f < (wt + 1) * (D0 / 2); ++f) E[f * kLD + s] = (s < ns && f < D) ? sr[f] : 0.f;
+        if (wt == 0) tS[s] = s < ns ? stg[LY::kStEnc + s] : 0.f;
+        if (wt == 1 && s < nr) {
+          float* t8 = sTg + s * kTgt;
+          const float* tg = stg + LY::kStTg + 4 * s;
+          t8[0] = tg[0];
+          t8[1] = tg[1];
+          t8[2] = tg[2];
+          t8[3] = tg[3];
+          const int rg = int(reinterpret_cast<uintptr_t>(st.tmask + int64_t(k) * st.R + r_begin) & 3) + s;
+          const uint8_t* fl = reinterpret_cast<const uint8_t*>(stg + LY::kStFl);
+          // each array's words were copied from its own aligned base
+          const int rv = int(reinterpret_cast<uintptr_t>(st.valid + int64_t(k) * st.R + r_begin) & 3) + s;
+          const int ro = int(reinterpret_cast<uintptr_t>(st.ok + int64_t(k) * st.R + r_begin) & 3) + s;
+          t8[4] = fl[rg] != 0 ? 1.f : 0.f;
+          t8[5] = fl[4 * LY::kFw + rv] != 0 ? 1.f : 0.f;
+          t8[6] = fl[8 * LY::kFw + ro] != 0 ? 1.f : 0.f;
+        }
+      } else if (st.pts) {
         float pc[3] = {0.f, 0.f, 0.f};
         if (s < ns) {
 #pragma unroll
@@ -369,8 +408,8 @@ __global__ void __launch_bounds__(NTHR, 2) kf32_train_kernel(const __grid_consta
             E[ff * kLD + ns + (idx - ff * np_)] = 0.f;
           }
       }
-      if (wt == 0) tS[s] = s < ns ? st.t[gs0 + s] : 0.f;
-      if (wt == 1 && s < nr) {  // this block's ray targets, read early (the render needs them mid-block)
+      if (!pf && wt == 0) tS[s] = s < ns ? st.t[gs0 + s] : 0.f;
+      if (!pf && wt == 1 && s < nr) {  // this block's ray targets, read early (the render needs them mid-block)
         const int64_t rg = int64_t(k) * st.R + r_begin + s;
         float* t8 = sTg + s * kTgt;
         t8[0] = st.tdepth[rg];
@@ -431,7 +470,7 @@ __global__ void __launch_bounds__(NTHR, 2) kf32_train_kernel(const __grid_consta
         tg.ok = t8[6] != 0.f;
         RayLossGrad lg;
         if constexpr (SFIX > 0) {
-          lg = render_ray_smem<SFIX>(O, tS, sb, tg, st.wc, st.wo);
+          lg = render_ray_smem<SFIX, kLD>(O, tS, sb, tg, st.wc, st.wo);
         } else {
           float* Tsc = tS + kSB;
           auto occ = [&](int i) { return O[sb + i]; };
@@ -461,6 +500,8 @@ __global__ void __launch_bounds__(NTHR, 2) kf32_train_kernel(const __grid_consta
 #pragma unroll
         for (int cc = 0; cc < 4; ++cc) O[cc * kLD + lane] = 0.f;
       }
+    } else if (pf && blk + NT < blk1) {
+      prefetch(blk + NT);  // the staging area was consumed at this block's start
     }
     team_bar(team);
 
@@ -618,16 +659,17 @@ bool kf32_supported(const KParams& p) {
   return true;
 }
 
-size_t kf32_smem_bytes() { return kf32::kSmemBytes; }
+size_t kf32_smem_bytes() { return kf32::Lay<10>::kSmem > kf32::Lay<0>::kSmem ? kf32::Lay<10>::kSmem : kf32::Lay<0>::kSmem; }
 
 int launch_kf32(const KParams& p, int grid, cudaStream_t s) {
   bool all10 = true;
   for (int i = 0; i < p.n_stacks; ++i) all10 &= p.s[i].S == 10;
   const void* fn = all10 ? reinterpret_cast<const void*>(kf32::kf32_train_kernel<10>)
                          : reinterpret_cast<const void*>(kf32::kf32_train_kernel<0>);
-  VM_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kf32::kSmemBytes)));
+  const size_t smem = all10 ? kf32::Lay<10>::kSmem : kf32::Lay<0>::kSmem;
+  VM_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   void* args[] = {const_cast<KParams*>(&p)};
-  VM_CUDA(cudaLaunchKernel(fn, dim3(grid), dim3(kf32::NTHR), args, kf32::kSmemBytes, s));
+  VM_CUDA(cudaLaunchKernel(fn, dim3(grid), dim3(kf32::NTHR), args, smem, s));
   return VM_OK;
 }
 

@@ -699,6 +699,19 @@ bool kf32_enabled() {
   return on;
 }
 
+// VM_KH=1 runs hidden-32 object stacks on the warp-level tensor path (KH32,
+// 3xTF32 mma.sync) instead of the FP32 FFMA kernel KF32.  Off by default:
+// measured on B200 at config 2 it is no faster standalone (65.6 vs 65.1 us,
+// ncu) and its one-CTA-per-SM footprint slows the concurrent KT phase
+// (0.183 vs 0.175 ms/step); see DESIGN.md "KH32".
+bool kh32_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("VM_KH");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
 // The tensor-core path is the default for hidden-128 stacks; VM_TC=0 selects
 // the FFMA kernel for them (A/B measurements and the parity cross-check).
 bool tc_enabled() {
@@ -902,6 +915,7 @@ extern "C" int vm_train_step(const VmStack* stacks, const VmBatch* batches, int 
     ks.item_base = ff_grid;
     ff_grid += ks.items ? ks.n_items : ks.K * ks.P;
   }
+  const bool use_kh32 = use_kf32 && kh32_enabled() && kh32_supported(kf);
   if (kf.n_stacks > 0 && !use_kf32) {
     fn = pick_kernel<kTrain>(kf.s[0].H, kf.s[0].L, kf.n_stacks > 1 ? kf.s[1].H : 0, kf.n_stacks > 1 ? kf.s[1].L : 0);
   }
@@ -954,7 +968,8 @@ extern "C" int vm_train_step(const VmStack* stacks, const VmBatch* batches, int 
       g_prof.pair(kf0, kf1, 1);
       VM_CUDA(cudaEventRecord(kf0, s));
     }
-    const int r = use_kf32 ? launch_kf32(kf, ff_grid, s) : launch_mlp(fn, kf, ff_grid, pl.smem, s);
+    const int r = use_kf32 ? (use_kh32 ? launch_kh32(kf, ff_grid, s) : launch_kf32(kf, ff_grid, s))
+                           : launch_mlp(fn, kf, ff_grid, pl.smem, s);
     if (r) return r;
     if (g_prof.on) {
       g_prof.kernels += 1;

@@ -104,6 +104,9 @@ struct KParams {
 bool kf32_supported(const KParams& p);
 size_t kf32_smem_bytes();
 int launch_kf32(const KParams& p, int grid, cudaStream_t s);
+// vm_kh32.cu: the same step on the warp-level tensor path (3xTF32 mma.sync)
+bool kh32_supported(const KParams& p);
+int launch_kh32(const KParams& p, int grid, cudaStream_t s);
 
 __device__ __forceinline__ void team_sync(int team, int T) {
   if (T == 1) {

@@ -186,4 +186,56 @@ __device__ __forceinline__ RayLossGrad render_ray_fixed(float (&o)[NS], float (&
   return lg;
 }
 
+// Register-light render chain for one ray (render_ray_fixed's operation
+// order): occupancy/colour/t are read from smem (feature-major rows of LD
+// floats: occupancy, r, g, b), the 2*NS transmittance and
+// weight values stay in registers; writes dz (sigmoid'd gradients) in place.
+template <int NS, int LD>
+__device__ __forceinline__ RayLossGrad render_ray_smem(float* __restrict__ O, const float* __restrict__ tS, int sb,
+                                                       const RayTargets& tg, float w_colour, float w_occ) {
+  float Tr[NS], w[NS];
+  float Tc = 1.0f;
+#pragma unroll
+  for (int i = 0; i < NS; ++i) {
+    const float o = O[sb + i];
+    Tr[i] = Tc;
+    Tc = (i == 0) ? __fsub_rn(1.0f, o) : __fmul_rn(Tc, __fsub_rn(1.0f, o));
+    w[i] = __fmul_rn(o, Tr[i]);
+  }
+  RayFwd f;
+  f.opacity = pairwise_sum_fixed<NS>([&](int i) { return w[i]; });
+  f.depth = pairwise_sum_fixed<NS>([&](int i) { return __fmul_rn(w[i], tS[sb + i]); });
+#pragma unroll
+  for (int ch = 0; ch < 3; ++ch) {
+    const float* c = O + (1 + ch) * LD + sb;
+    float acc = __fmul_rn(w[0], c[0]);
+#pragma unroll
+    for (int i = 1; i < NS; ++i) acc = __fadd_rn(acc, __fmul_rn(w[i], c[i]));
+    f.colour[ch] = acc;
+  }
+  const RayLossGrad lg = ray_loss_grad(f, tg, w_colour, w_occ);
+  float rev = 0.0f;
+#pragma unroll
+  for (int i = NS - 1; i >= 0; --i) {
+    float cl[3];
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) cl[ch] = O[(1 + ch) * LD + sb + i];
+    float cs = __fmul_rn(lg.dC[0], cl[0]);
+    cs = __fadd_rn(cs, __fmul_rn(lg.dC[1], cl[1]));
+    cs = __fadd_rn(cs, __fmul_rn(lg.dC[2], cl[2]));
+    const float g = __fadd_rn(__fadd_rn(lg.dO, __fmul_rn(lg.dD, tS[sb + i])), cs);
+    const float gw = __fmul_rn(g, w[i]);
+    rev = (i == NS - 1) ? gw : __fadd_rn(rev, gw);
+    const float suffix = __fsub_rn(rev, gw);
+    const float oi = O[sb + i];
+    const float denom = np_maximum(__fsub_rn(1.0f, oi), 1e-7f);
+    const float d_occ = __fsub_rn(__fmul_rn(g, Tr[i]), __fdiv_rn(suffix, denom));
+    O[sb + i] = __fmul_rn(__fmul_rn(d_occ, oi), __fsub_rn(1.0f, oi));
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch)
+      O[(1 + ch) * LD + sb + i] = __fmul_rn(__fmul_rn(__fmul_rn(w[i], lg.dC[ch]), cl[ch]), __fsub_rn(1.0f, cl[ch]));
+  }
+  return lg;
+}
+
 }  // namespace vm

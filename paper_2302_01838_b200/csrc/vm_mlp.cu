@@ -820,9 +820,11 @@ int launch_reduce(const TrainPlan& pl, int i, cudaStream_t s) {
 
 // One Adam launch over every stack.  Adam of stack i reads the status words
 // of stacks < i (trainer.py:368-388 raise order).
-int launch_adam(const TrainPlan& pl, cudaStream_t s) {
-  if (pl.adam_grid <= 0) return VM_OK;
-  adam_train_kernel<<<pl.adam_grid, 256, 0, s>>>(pl.ap, 0);
+// Adam over the CTA range [b0, b1) of the plan's Adam grid (stack order).
+int launch_adam(const TrainPlan& pl, cudaStream_t s, int b0 = 0, int b1 = -1) {
+  if (b1 < 0) b1 = pl.adam_grid;
+  if (b1 <= b0) return VM_OK;
+  adam_train_kernel<<<b1 - b0, 256, 0, s>>>(pl.ap, b0);
   VM_CUDA(cudaGetLastError());
   if (g_prof.on) g_prof.kernels += 1;
   return VM_OK;
@@ -935,9 +937,11 @@ extern "C" int vm_train_step(const VmStack* stacks, const VmBatch* batches, int 
   }
   // The tensor-core stacks run on a side stream, concurrently with the FFMA
   // kernel (fork/join with events; both are captured when `s` is capturing).
-  // Their weight images are built on `s` before the fork; the FFMA kernel is
-  // launched right after the fork, then KT, whose one-tile-per-SM CTAs take
-  // the SMs the first FFMA wave leaves and those it frees.
+  // The FFMA kernel is launched right after the fork (then the FFMA stacks'
+  // Adam, on the caller's stream); the branch builds KT's pre-split weight
+  // image (tc_prep_kernel) and runs KT, whose one-tile-per-SM CTAs take the
+  // SMs the first FFMA wave leaves and those it frees, then the partial
+  // reduce; the remaining Adam runs after the join.
   // side stream + fork/join events: one set per (host thread, device), so
   // concurrent callers on different threads or devices never share them
   struct SideRes {
@@ -954,14 +958,23 @@ extern "C" int vm_train_step(const VmStack* stacks, const VmBatch* batches, int 
   bool forked = false;
   cudaStream_t ts = s;
   using TI = tck::Img<128, 4>;
-  for (int i = 0; i < n_stacks; ++i) {
+  auto launch_prep = [&](int i, cudaStream_t st) -> int {
     const KStack& ks = pl.kp.s[i];
-    if (!ks.tc || ks.K == 0) continue;
     float* img = reinterpret_cast<float*>(ws + pl.off_img[i]);
-    tck::tc_prep_kernel<128, 4><<<dim3(TI::n_chunks * 4, ks.K), 256, 0, s>>>(ks, img);
+    tck::tc_prep_kernel<128, 4><<<dim3(TI::n_chunks * 4, ks.K), 256, 0, st>>>(ks, img);
     VM_CUDA(cudaGetLastError());
     if (g_prof.on) g_prof.kernels += 1;
-  }
+    return VM_OK;
+  };
+  // Adam of the leading FFMA stacks can run on the caller's stream as soon
+  // as KF is done, overlapping the tensor-core branch (their updates never
+  // depend on a later stack's status); the rest runs after the join.
+  int adam_split = 0;
+  for (int i = 0; i < n_stacks && !pl.kp.s[i].tc; ++i)
+    adam_split = (i + 1 < n_stacks) ? pl.ap.s[i + 1].item_base : pl.adam_grid;
+  bool any_tc = false;
+  for (int i = 0; i < n_stacks; ++i) any_tc |= pl.kp.s[i].tc && pl.kp.s[i].K > 0;
+  if (!any_tc) adam_split = 0;
   auto launch_kf = [&]() -> int {
     if (!fn && !use_kf32) return VM_OK;
     if (g_prof.on) {
@@ -975,7 +988,7 @@ extern "C" int vm_train_step(const VmStack* stacks, const VmBatch* batches, int 
       g_prof.kernels += 1;
       VM_CUDA(cudaEventRecord(kf1, s));
     }
-    return VM_OK;
+    return launch_adam(pl, s, 0, adam_split);
   };
   // launch order: the FFMA kernel goes first (measured 0.195 vs 0.207 ms per
   // graph-replayed config-2 step); VM_KT_FIRST=1 launches KT first instead
@@ -1014,6 +1027,8 @@ extern "C" int vm_train_step(const VmStack* stacks, const VmBatch* batches, int 
       g_prof.pair(kt0, kt1, 2);
       VM_CUDA(cudaEventRecord(kt0, ts));
     }
+    rc = launch_prep(i, ts);
+    if (rc) return rc;
     float* img = reinterpret_cast<float*>(ws + pl.off_img[i]);
     const int smem_tc = tck::Smem<128, 4>::total;
     VM_CUDA(cudaFuncSetAttribute(tck::tc_train_kernel<128, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_tc));
@@ -1038,7 +1053,7 @@ extern "C" int vm_train_step(const VmStack* stacks, const VmBatch* batches, int 
     g_prof.pair(r0, r1, 3);
     VM_CUDA(cudaEventRecord(r0, s));
   }
-  rc = launch_adam(pl, s);
+  rc = launch_adam(pl, s, adam_split);
   if (rc) return rc;
   if (r1) VM_CUDA(cudaEventRecord(r1, s));
   return VM_OK;

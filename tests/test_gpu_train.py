@@ -69,17 +69,23 @@ def test_rayless_and_frozen_models_untouched(cuda):
     assert state.step[:3].cpu().tolist() == [3, 0, 2]
 
 
-def test_vectorised_matches_sequential(cuda):
-    arch = ModelArch(n_layers=3, hidden=16, n_freq=3)
-    pv, sv = init_stacked(arch, 3, seed=11)
-    ps, ss = init_stacked(arch, 3, seed=11)
-    batch = _synthetic_batch(arch, 3, 24, 6, seed=7)
+@pytest.mark.parametrize("hidden,n_layers,n_freq,k,rays,points", [
+    (16, 3, 3, 3, 24, 6),      # generic FFMA kernel
+    (32, 4, 5, 5, 120, 10),    # KF32 (the reference's object model), 5 chunks per model
+    (32, 4, 5, 4, 37, 10)])    # KF32, partial last block and chunk
+def test_vectorised_matches_sequential(cuda, hidden, n_layers, n_freq, k, rays, points):
+    """test_trainer.py:117-132: one launch over K models == K launches of
+    one model, bit for bit (the work split depends on a model's own rays)."""
+    arch = ModelArch(n_layers=n_layers, hidden=hidden, n_freq=n_freq)
+    pv, sv = init_stacked(arch, k, seed=11)
+    ps, ss = init_stacked(arch, k, seed=11)
+    batch = _synthetic_batch(arch, k, rays, points, seed=7)
     for _ in range(5):
         lv = train_on_batch(pv, sv, batch, LossWeights())
         ls = train_on_batch_sequential(ps, ss, batch, LossWeights())
         for a, b in zip(lv, ls):
             np.testing.assert_array_equal(a, b.astype(np.float32))
-    assert torch.equal(pv.arena[:3], ps.arena[:3])
+    assert torch.equal(pv.arena[:k], ps.arena[:k])
 
 
 def test_nonfinite_gradient_raises_and_skips_update(cuda):
@@ -149,3 +155,47 @@ def test_tensor_core_partial_tiles_and_sample_counts(cuda, k, rays, points):
         np.testing.assert_allclose(lo, eo, rtol=1e-4, atol=1e-6)
     assert_params_rel_l2(params, ost)
     np.testing.assert_array_equal(state.step[:k].cpu().numpy(), ost.step[:k])
+
+
+KH32_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+from oracle import vobj_oracle as O
+from paper_2302_01838_b200 import LossWeights, ModelArch, init_stacked, train_on_batch
+from paper_2302_01838_b200.trainer import _synthetic_batch, train_on_batch_sequential
+from tests.helpers import assert_params_rel_l2, oracle_arch, to_host_batch
+arch = ModelArch(n_layers=4, hidden=32, n_freq=5)
+k = 5
+params, state = init_stacked(arch, k, seed=11)
+ps, ss = init_stacked(arch, k, seed=11)
+ost = O.new_stack(oracle_arch(arch), k, 11)
+batch = _synthetic_batch(arch, k, 120, 10, seed=7)
+hb = to_host_batch(batch)
+for step in range(5):
+    got = train_on_batch(params, state, batch, LossWeights())
+    seq = train_on_batch_sequential(ps, ss, batch, LossWeights())
+    for a, b in zip(got, seq):
+        np.testing.assert_array_equal(a, b.astype(np.float32))
+    exp = O.train_on_batch(ost, hb)
+    for a, e in zip(got, exp):
+        np.testing.assert_allclose(a, e, rtol=1e-4, atol=1e-6)
+assert torch.equal(params.arena[:k], ps.arena[:k])
+assert_params_rel_l2(params, ost)
+print("kh32 ok")
+"""
+
+
+def test_kh32_tensor_path_opt_in(cuda):
+    """VM_KH=1: hidden-32 objects on the 3xTF32 mma.sync kernel (KH32).
+    Losses within rtol 1e-4 of the oracle for 5 steps, vectorised ==
+    sequential bit for bit, and the 3xTF32 parameter contract (per-object
+    relative L2 <= 1e-4, as for the tensor-core background kernel)."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    env = dict(os.environ, VM_KH="1")
+    r = subprocess.run([sys.executable, "-c", KH32_SCRIPT, str(root)], env=env, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0 and "kh32 ok" in r.stdout, r.stdout + r.stderr

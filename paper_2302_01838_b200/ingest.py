@@ -18,7 +18,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .geometry import AABB, aabb_iou
+from .geometry import AABB
 from .objects import AssociationConfig, ObjectInstance, ObjectMap
 from .render import CameraIntrinsics
 
@@ -123,23 +123,40 @@ def extract_detections_device(ing: FrameIngestor, frame: Frame, intr: CameraIntr
 
 def associate(detections: list, object_map: ObjectMap, cfg: AssociationConfig) -> list:
     """objects.py:233-259: greedy one-to-one matching by descending 3D IoU
-    (ties: lower object id, then lower detection index)."""
-    candidates = []
-    for det_idx, det in enumerate(detections):
-        for inst in object_map.objects():
-            if inst.semantic_class != det.semantic_class:
-                continue
-            iou = aabb_iou(det.aabb, inst.aabb)
-            if iou >= cfg.iou_threshold:
-                candidates.append((-iou, inst.object_id, det_idx))
-    candidates.sort()
+    (ties: lower object id, then lower detection index).  The detection x
+    object IoU matrix is formed in one vectorised pass with aabb_iou's
+    operation order (per-axis max/min, the product x*y*z, (va + vb) - inter),
+    so every IoU -- and hence the match -- is bit-identical to the pairwise
+    loop; only the candidates that pass the threshold are sorted."""
+    objs = list(object_map.objects())
+    if not detections or not objs:
+        return [None] * len(detections)
+    dmin = np.stack([np.asarray(d.aabb.min, np.float64) for d in detections])[:, None, :]
+    dmax = np.stack([np.asarray(d.aabb.max, np.float64) for d in detections])[:, None, :]
+    omin = np.stack([np.asarray(o.aabb.min, np.float64) for o in objs])[None, :, :]
+    omax = np.stack([np.asarray(o.aabb.max, np.float64) for o in objs])[None, :, :]
+    lo = np.maximum(dmin, omin)
+    hi = np.minimum(dmax, omax)
+    overlap = ~np.any(hi <= lo, axis=-1)
+    inter = np.prod(hi - lo, axis=-1)
+    vd = np.prod(dmax - dmin, axis=-1)
+    vo = np.prod(omax - omin, axis=-1)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        iou = np.where(overlap, inter / ((vd + vo) - inter), 0.0)
+    dcls = np.array([d.semantic_class for d in detections])[:, None]
+    ocls = np.array([o.semantic_class for o in objs])[None, :]
+    ok = (dcls == ocls) & (iou >= cfg.iou_threshold)
+    di, oi = np.nonzero(ok)
+    oid = np.array([o.object_id for o in objs])[oi]
+    order = np.lexsort((di, oid, -iou[di, oi]))  # key order: -iou, object id, detection index
     assigned = [None] * len(detections)
     used = set()
-    for _neg, obj_id, det_idx in candidates:
-        if assigned[det_idx] is not None or obj_id in used:
+    for j in order:
+        d, o = int(di[j]), int(oid[j])
+        if assigned[d] is not None or o in used:
             continue
-        assigned[det_idx] = obj_id
-        used.add(obj_id)
+        assigned[d] = o
+        used.add(o)
     return assigned
 
 

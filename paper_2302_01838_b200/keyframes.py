@@ -39,6 +39,37 @@ class KeyframeArena:
         mask[:self.used] = self.mask[:self.used]
         self.rgbd, self.mask = rgbd, mask
 
+    def add_many(self, kfs) -> None:
+        """Upload several keyframes' crops with one H2D copy per arena plane
+        (the per-frame ingestion path adds a few dozen at a time)."""
+        kfs = [kf for kf in kfs if getattr(kf, "texel_off", -1) < 0]
+        if len(kfs) <= 1:
+            for kf in kfs:
+                self.add(kf)
+            return
+        sizes = []
+        for kf in kfs:
+            u0, v0, u1, v1 = kf.bbox
+            h, w = v1 - v0, u1 - u0
+            if kf.rgb.shape[:2] != (h, w) or kf.depth.shape != (h, w) or kf.mask.shape != (h, w):
+                raise ValueError(f"keyframe crop shapes do not match bbox {kf.bbox}")
+            sizes.append(h * w)
+        total = int(sum(sizes))
+        self._reserve(total)
+        tex = np.empty((total, 4), np.float32)
+        msk = np.empty(total, np.uint8)
+        off = 0
+        for kf, n in zip(kfs, sizes):
+            tex[off:off + n, :3] = kf.rgb.reshape(n, 3)
+            tex[off:off + n, 3] = kf.depth.reshape(n)
+            msk[off:off + n] = kf.mask.reshape(n)
+            kf.texel_off = self.used + off
+            off += n
+        base = self.used
+        self.rgbd[base:base + total] = torch.from_numpy(tex).to(self.device)
+        self.mask[base:base + total] = torch.from_numpy(msk).to(self.device)
+        self.used += total
+
     def add(self, kf) -> int:
         """Upload one Keyframe's crops; records kf.texel_off and returns it."""
         u0, v0, u1, v1 = kf.bbox
@@ -115,11 +146,10 @@ def build_tables(arena: KeyframeArena, instances, bound_pad: float, frozen=None,
     objs = np.zeros(max(n, 1), OBJ_DTYPE)
     parts = []
     n_kf, mins, maxs, ids, active, scale, rays = [], [], [], [], [], [], []
+    arena.add_many([kf for inst in instances for kf in inst.keyframes if getattr(kf, "texel_off", -1) < 0])
     for k, inst in enumerate(instances):
         kfs = inst.keyframes
         for kf in kfs:
-            if getattr(kf, "texel_off", -1) < 0:
-                arena.add(kf)
             parts.append(_kf_desc(kf))
         n_kf.append(len(kfs))
         mins.append(inst.aabb.min)

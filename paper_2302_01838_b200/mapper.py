@@ -105,8 +105,7 @@ class Mapper:
 
     def add_keyframe(self, inst, frame_id, pose, bbox, mask, rgb, depth):
         kf = add_keyframe(inst, frame_id, pose, bbox, mask, rgb, depth)
-        self.arena.add(kf)
-        self.invalidate()
+        self.invalidate()  # the crop is uploaded with the frame's others at the next table build
         return kf
 
     # ------------------------------------------------------------ ingestion

@@ -80,3 +80,47 @@ def test_pack_unpack_model():
     unpack_model(buf, a2, m2, v2, s2, 1)
     assert torch.equal(a2[1], arena[2]) and torch.equal(m2[1], m[2]) and torch.equal(v2[1], v[2])
     assert int(s2[1]) == 123456789
+
+
+def test_associate_vectorised_matches_pairwise_loop():
+    """ingest.associate (one IoU matrix) == the pairwise loop of
+    objects.py:233-259 on random boxes with shared classes and exact ties."""
+    from types import SimpleNamespace
+
+    from paper_2302_01838_b200.geometry import AABB, aabb_iou
+    from paper_2302_01838_b200.ingest import associate
+    from paper_2302_01838_b200.objects import AssociationConfig
+
+    def loop(dets, objs, thr):
+        cand = []
+        for di, d in enumerate(dets):
+            for o in objs:
+                if o.semantic_class != d.semantic_class:
+                    continue
+                iou = aabb_iou(d.aabb, o.aabb)
+                if iou >= thr:
+                    cand.append((-iou, o.object_id, di))
+        cand.sort()
+        out, used = [None] * len(dets), set()
+        for _, oid, di in cand:
+            if out[di] is None and oid not in used:
+                out[di] = oid
+                used.add(oid)
+        return out
+
+    g = np.random.default_rng(3)
+    for trial in range(20):
+        def box():
+            lo = g.uniform(-2, 2, 3)
+            return AABB(lo, lo + g.uniform(0.05, 1.5, 3))
+        objs = [SimpleNamespace(object_id=int(i * 3 + 1), semantic_class=int(g.integers(1, 3)), aabb=box())
+                for i in range(int(g.integers(0, 40)))]
+        dets = [SimpleNamespace(semantic_class=int(g.integers(1, 3)), aabb=box()) for _ in range(int(g.integers(0, 30)))]
+        if objs and dets:  # an exact duplicate box: tie on IoU
+            dets[0].aabb = AABB(objs[0].aabb.min.copy(), objs[0].aabb.max.copy())
+            dets[0].semantic_class = objs[0].semantic_class
+        omap = SimpleNamespace(objects=lambda objs=objs: iter(objs))
+        cfg = AssociationConfig()
+        for thr in (cfg.iou_threshold, 0.01):
+            c = AssociationConfig(iou_threshold=thr)
+            assert associate(dets, omap, c) == loop(dets, objs, thr), trial

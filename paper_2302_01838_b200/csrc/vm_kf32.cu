@@ -25,6 +25,8 @@
 //    the chunk that finishes last (atomic ticket) sums the partials in chunk
 //    order and finalises the model (loss sums in numpy's pairwise order,
 //    update mask, non-finite flags) -- no separate reduce kernel.
+#include <algorithm>
+
 #include "vm_mlp.cuh"
 
 namespace vm {
@@ -208,9 +210,8 @@ __device__ __forceinline__ void team_bar(int team) {
 }
 
 template <int SFIX>
-__global__ void __launch_bounds__(NTHR, 2) kf32_train_kernel(const __grid_constant__ KParams p) {
-  extern __shared__ __align__(16) float smem[];
-  int item = blockIdx.x, si = 0;
+__device__ __forceinline__ void train_item(const KParams& p, int item, float* smem) {
+  int si = 0;
   if (p.n_stacks > 1 && item >= p.s[1].item_base) si = 1;
   const KStack& st = p.s[si];
   item -= st.item_base;
@@ -648,6 +649,27 @@ __global__ void __launch_bounds__(NTHR, 2) kf32_train_kernel(const __grid_consta
   finalize_model(st, k, all_finite, true, smem + kWFloats, NT * kTeamFloats);
 }
 
+// One CTA per work item, or (p.queue set) a persistent grid whose CTAs pull
+// items from an atomic counter: which CTA trains an item never changes its
+// bits (the item's blocks, team order and partial slot are fixed by the item).
+template <int SFIX>
+__global__ void __launch_bounds__(NTHR, 2) kf32_train_kernel(const __grid_constant__ KParams p) {
+  extern __shared__ __align__(16) float smem[];
+  if (!p.queue) {
+    train_item<SFIX>(p, blockIdx.x, smem);
+    return;
+  }
+  __shared__ int s_item;
+  for (;;) {
+    if (threadIdx.x == 0) s_item = atomicAdd(p.queue, 1);
+    __syncthreads();
+    const int item = s_item;
+    if (item >= p.n_items) break;
+    train_item<SFIX>(p, item, smem);
+    __syncthreads();  // smem (weights, team regions, s_item) free for the next item
+  }
+}
+
 }  // namespace kf32
 
 // True when every stack of the launch fits the specialised kernel.
@@ -668,7 +690,15 @@ int launch_kf32(const KParams& p, int grid, cudaStream_t s) {
                          : reinterpret_cast<const void*>(kf32::kf32_train_kernel<0>);
   const size_t smem = all10 ? kf32::Lay<10>::kSmem : kf32::Lay<0>::kSmem;
   VM_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-  void* args[] = {const_cast<KParams*>(&p)};
+  KParams q = p;
+  if (q.queue) {  // persistent: two CTAs per SM pull the items
+    static int sms = 0;
+    if (!sms) VM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+    q.n_items = grid;
+    grid = std::min(grid, 2 * sms);
+    VM_CUDA(cudaMemsetAsync(q.queue, 0, sizeof(int), s));
+  }
+  void* args[] = {&q};
   VM_CUDA(cudaLaunchKernel(fn, dim3(grid), dim3(kf32::NTHR), args, smem, s));
   return VM_OK;
 }

@@ -685,6 +685,7 @@ struct TrainPlan {
   size_t ws_bytes;
   // workspace offsets
   size_t off_grads[2], off_part[2], off_terms[2], off_cnt[2], off_upd[2], off_corr[2], off_img[2];
+  size_t off_queue;
 };
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
@@ -794,6 +795,8 @@ int plan_train(const VmStack* stacks, const VmBatch* batches, int n, TrainPlan& 
     as.a = adam_consts(stacks[i]);
     adam_base += ks.K * as.chunks;
   }
+  pl.off_queue = off;
+  off = align_up(off + 4, 256);
   pl.grid = item_base;
   pl.adam_grid = adam_base;
   pl.ws_bytes = off;
@@ -899,6 +902,14 @@ extern "C" int vm_train_step(const VmStack* stacks, const VmBatch* batches, int 
   // FFMA kernel over the stacks KT does not take
   KParams kf;
   std::memset(&kf, 0, sizeof(kf));
+  // The FFMA object kernel runs as a persistent grid (two CTAs per SM) pulling
+  // work items from a counter: measured 0.171 vs 0.182 ms per config-2 step
+  // against one CTA per item; VM_KF_PERSIST=0 restores the latter.
+  static const bool kf_persist = [] {
+    const char* e = std::getenv("VM_KF_PERSIST");
+    return !(e && e[0] == '0');
+  }();
+  if (kf_persist) kf.queue = reinterpret_cast<int*>(ws + pl.off_queue);
   int ff_grid = 0;
   for (int i = 0; i < n_stacks; ++i) {
     if (pl.kp.s[i].tc) continue;
@@ -992,10 +1003,21 @@ extern "C" int vm_train_step(const VmStack* stacks, const VmBatch* batches, int 
   };
   // launch order: the FFMA kernel goes first (measured 0.195 vs 0.207 ms per
   // graph-replayed config-2 step); VM_KT_FIRST=1 launches KT first instead
-  static const bool kf_first = [] {
+  // VM_KT_FIRST=2: KT's weight image is built on the caller's stream before
+  // the fork, so KT and KF become ready together and KT (launched first)
+  // takes its SMs before KF's CTAs fill the rest
+  static const int kt_first_mode = [] {
     const char* e = std::getenv("VM_KT_FIRST");
-    return !(e && e[0] == '1');
+    return e ? std::atoi(e) : 0;
   }();
+  const bool kf_first = kt_first_mode == 0;
+  const bool prep_before_fork = kt_first_mode == 2;
+  if (prep_before_fork)
+    for (int i = 0; i < n_stacks; ++i)
+      if (pl.kp.s[i].tc && pl.kp.s[i].K > 0) {
+        rc = launch_prep(i, s);
+        if (rc) return rc;
+      }
   bool kf_done = false;
   for (int i = 0; i < n_stacks; ++i) {
     const KStack& ks = pl.kp.s[i];
@@ -1027,8 +1049,10 @@ extern "C" int vm_train_step(const VmStack* stacks, const VmBatch* batches, int 
       g_prof.pair(kt0, kt1, 2);
       VM_CUDA(cudaEventRecord(kt0, ts));
     }
-    rc = launch_prep(i, ts);
-    if (rc) return rc;
+    if (!prep_before_fork) {
+      rc = launch_prep(i, ts);
+      if (rc) return rc;
+    }
     float* img = reinterpret_cast<float*>(ws + pl.off_img[i]);
     const int smem_tc = tck::Smem<128, 4>::total;
     VM_CUDA(cudaFuncSetAttribute(tck::tc_train_kernel<128, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_tc));

@@ -98,6 +98,8 @@ struct KStack {
 struct KParams {
   KStack s[2];
   int n_stacks;
+  int* queue;      // persistent FFMA kernel: next work item (zeroed before the launch), or null
+  int n_items;     // work items over all stacks (persistent kernel)
 };
 
 // vm_kf32.cu: the specialised hidden-32 / 4-layer train kernel

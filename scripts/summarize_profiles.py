@@ -23,10 +23,10 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "sm__inst_executed_pipe_uniform.avg.pct_of_peak_sustained_active"]
 
 
-def raw(rep):
+def raw(rep, launch=0):
     txt = subprocess.run(["ncu", "-i", str(rep), "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(txt.splitlines()))
-    hdr, units, vals = rows[0], rows[1], rows[2]
+    hdr, units, vals = rows[0], rows[1], rows[2 + launch]
     return {k: (v, u) for k, u, v in zip(hdr, units, vals)}
 
 
@@ -43,14 +43,22 @@ lines = [f"# ncu summary ({tag})", "",
          "(KT and KF normally run concurrently on two streams; ncu serialises them).",
          "ncu flushes caches before each replay: durations are cold-cache and serialised.", ""]
 traffic = {}
-for name, rep in (("tensor-core MLP train (KT, tc_train_kernel, hidden-128 background)", "prof_tc"),
-                  ("FFMA MLP train (KF, mlp_kernel, hidden-32 objects)", "prof_mlp"),
-                  ("partial-gradient reduce (reduce_partials_kernel)", "prof_red"),
-                  ("sampler rays (KS)", "prof_rays"), ("Adam (KA)", "prof_adam")):
+for name, rep, launch in (("tensor-core MLP train (KT, tc_train_kernel, hidden-128 background)", "prof_tc", 0),
+                          ("FFMA MLP train (KF32, kf32_train_kernel, hidden-32 objects)", "prof_kf32", 0),
+                          ("FFMA MLP train (KF, mlp_kernel, generic)", "prof_mlp", 0),
+                          ("opt-in tensor path for the objects (KH32, kh32_train_kernel, 3xTF32 mma.sync)",
+                           "prof_kh32", 0),
+                          ("partial-gradient reduce (reduce_partials_kernel)", "prof_red", 0),
+                          ("sampler prep, objects (KS, sample_prep_kernel grid 50)", "prof_prep", 0),
+                          ("sampler prep, background (KS, sample_prep_kernel grid 1)", "prof_prep", 1),
+                          ("sampler rays (KS)", "prof_rays", 0), ("Adam (KA)", "prof_adam", 0)):
     p = ROOT / "gpurun_out" / f"{rep}.ncu-rep"
     if not p.exists():
         continue
-    d = raw(p)
+    try:
+        d = raw(p, launch)
+    except IndexError:
+        continue
     lines += [f"## {name}", "", "| metric | value | unit |", "|---|---|---|"]
     for k in KEYS:
         if k in d:
@@ -59,11 +67,11 @@ for name, rep in (("tensor-core MLP train (KT, tc_train_kernel, hidden-128 backg
               ", ".join(f"{k} {v:.1f}%" for k, v in stalls(d)), ""]
     mb = lambda k: float(d[k][0].replace(",", "")) * (1e9 if d[k][1] == "Gbyte" else 1e6 if d[k][1] == "Mbyte"
                                                       else 1e3 if d[k][1] == "Kbyte" else 1)
-    if rep in ("prof_mlp", "prof_tc"):
-        key = "mlp_kernel_dram_bytes_per_launch" if rep == "prof_mlp" else "tc_train_kernel_dram_bytes_per_launch"
+    if rep in ("prof_kf32", "prof_tc"):
+        key = "mlp_kernel_dram_bytes_per_launch" if rep == "prof_kf32" else "tc_train_kernel_dram_bytes_per_launch"
         traffic[key] = mb("dram__bytes_read.sum") + mb("dram__bytes_write.sum")
         traffic["source"] = f"profiles/{tag}_summary.md (ncu --set full, cold cache)"
-summ = ROOT / "gpurun_out" / "launches_summary.txt"
+summ = ROOT / "gpurun_out" / f"{tag}_launches.txt"
 if summ.exists():
     lines += ["## Launch list (ncu --metrics gpu__time_duration.sum, per-step kernels)", "", "```",
               summ.read_text().rstrip(), "```", ""]

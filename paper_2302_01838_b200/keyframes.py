@@ -118,9 +118,15 @@ class DeviceTable:
         self.buf = None
         self.pinned = None
         self.done = None   # event after the last staging copy
+        self.last = None   # bytes of the last upload
+        self.changed = True
 
     def upload(self, raw: bytes) -> torch.Tensor:
         n = len(raw)
+        self.changed = raw != self.last
+        if not self.changed:  # identical table: nothing to copy (map refreshes without edits)
+            return self.buf
+        self.last = raw
         if self.buf is None or self.buf.numel() < n:
             cap = max(256, 1 << (n - 1).bit_length())
             self.buf = torch.zeros(cap, dtype=torch.uint8, device=self.device)
@@ -146,11 +152,22 @@ def build_tables(arena: KeyframeArena, instances, bound_pad: float, frozen=None,
     objs = np.zeros(max(n, 1), OBJ_DTYPE)
     parts = []
     n_kf, mins, maxs, ids, active, scale, rays = [], [], [], [], [], [], []
-    arena.add_many([kf for inst in instances for kf in inst.keyframes if getattr(kf, "texel_off", -1) < 0])
+    # per-instance descriptor bytes are cached against the (append-only)
+    # keyframe list; only instances whose list grew are re-scanned for crops
+    # to upload
+    stale = []
+    for inst in instances:
+        c = getattr(inst, "_vm_kfb", None)
+        if c is None or c[0] is not inst.keyframes or c[1] != len(inst.keyframes):
+            stale.append(inst)
+    if stale:
+        arena.add_many([kf for inst in stale for kf in inst.keyframes if getattr(kf, "texel_off", -1) < 0])
+        for inst in stale:
+            kfs = inst.keyframes
+            inst._vm_kfb = (kfs, len(kfs), b"".join([_kf_desc(kf) for kf in kfs]))
     for k, inst in enumerate(instances):
         kfs = inst.keyframes
-        for kf in kfs:
-            parts.append(_kf_desc(kf))
+        parts.append(inst._vm_kfb[2])
         n_kf.append(len(kfs))
         mins.append(inst.aabb.min)
         maxs.append(inst.aabb.max)

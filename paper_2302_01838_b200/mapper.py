@@ -71,6 +71,8 @@ class Mapper:
         self._dirty = True
         self._pin_scale = None
         self._pin_done = None
+        self._last_scales = None
+        self._tables_gen = 0
         self._n_kf = 0
         self._ingest = None
 
@@ -208,6 +210,19 @@ class Mapper:
         # PE scales through one pinned staging buffer (non-blocking uploads)
         sc = np.array([float(i.pe_scale) for i in objs] + ([float(bg.pe_scale)] if bg is not None else []),
                       np.float32)
+        regraph = self._g is None
+        unchanged = (not regraph and all(not d.changed for pair in self._dev_tables for d in pair)
+                     and self._last_scales is not None and np.array_equal(sc, self._last_scales))
+        self._last_scales = sc
+        if unchanged:
+            # a refresh without edits (e.g. invalidate() after a frame that
+            # changed nothing): the tables, scales and the prefetched batch stay valid
+            self._tables = (t_obj, t_bg)
+            self._tables_gen += 1
+            self._sig = sig
+            self._dirty = False
+            self._io = (0, self._io[1])
+            return
         if self._pin_scale is None or self._pin_scale.numel() < max(len(sc), 1):
             self._pin_scale = torch.empty(max(len(sc), 64), dtype=torch.float32, pin_memory=True)
         if len(sc):
@@ -228,6 +243,7 @@ class Mapper:
                     a.pe_scale.copy_(b.pe_scale)
             self._g["next_ready"] = None  # tables changed: drop the prefetched batch
         self._tables = (t_obj, t_bg)
+        self._tables_gen += 1
         self._sig = sig
         self._dirty = False
         up = sum(t.numel() for tab in self._tables if tab is not None for t in tab) + 4 * (K + (bg is not None))
@@ -389,17 +405,26 @@ class Mapper:
         (no host sync).  Results land in pinned host memory when the stream
         reaches them."""
         self._sync()
-        if self._g is None or self._g["key"] != self._graph_key():
-            self._snapshot_for_graph_build()
-            self._build_graphs()
-            self._restore_after_graph_build()
+        # the full graph key (device pointers of every table and buffer) is
+        # re-derived only after a table rebuild; in between, model counts and
+        # arena pointers guard against growth outside the Mapper's API
+        quick = (self.obj_params.count, self.bg_params.count, self.obj_params.arena.data_ptr(),
+                 self.bg_params.arena.data_ptr(), self._tables_gen)
+        if self._g is None or self._g.get("quick") != quick:
+            if self._g is None or self._g["key"] != self._graph_key():
+                self._snapshot_for_graph_build()
+                self._build_graphs()
+                self._restore_after_graph_build()
+            self._g["quick"] = quick
         g = self._g
         p = step & 1
-        g["step_dev"].fill_(step)
+        if g.get("dev_step") != step:  # the graph bumps the device counter itself
+            g["step_dev"].fill_(step)
         if g["next_ready"] != step:  # no prefetched batch for this step: sample it now
             g["sample"](p, 0)
         g["graphs"][p].replay()
         g["next_ready"] = step + 1
+        g["dev_step"] = step + 1
         for params, _, _ in g["stacks"][p]:
             params.version += 1
         return g["stacks"][p]
@@ -469,6 +494,9 @@ class Mapper:
         else:
             stacks = []
         row = 0
+        w = self.cfg.loss_weights
+        wc, wo = w.colour, w.occupancy
+        total = 0
         for si, (params, _, _) in enumerate(stacks):
             is_bg = params is self.bg_params
             kk = params.count
@@ -479,11 +507,13 @@ class Mapper:
             if st[si, 1] < kk or not np.isfinite(vals).all():
                 bad = int(np.flatnonzero(~np.isfinite(vals).all(axis=1))[0])
                 raise FloatingPointError(f"non-finite loss for object {ids[bad]}")
-            report_losses.update(zip(ids, map(tuple, vals.astype(np.float64).tolist())))
+            rows = vals.astype(np.float64).tolist()
+            report_losses.update(zip(ids, map(tuple, rows)))
             row += kk
             k_models += kk
-        w = self.cfg.loss_weights
-        total = sum(d + w.colour * c + w.occupancy * o for d, c, o in report_losses.values())
+        # the reference's sum over report.losses.values() in insertion order
+        for d, c, o in report_losses.values():
+            total += d + wc * c + wo * o
         self.global_step += 1
         return StepReport(step=step, frame_id=self.last_frame_id, k_models=k_models, losses=report_losses,
                           total=float(total), ms=(time.perf_counter() - t0) * 1e3)

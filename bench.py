@@ -418,27 +418,38 @@ def main():
     value = k_total * args.steps / (total_ms / 1e3)
 
     # end-to-end through the public API: Mapper.train_step() per step (graph
-    # replay + one pinned D2H read of losses/status + StepReport), with the
-    # per-object sampling tables rebuilt and re-uploaded from host memory every
-    # cfg.steps_per_frame steps, the cadence at which run_mapping ingests a
-    # frame (trainer.py:554-561).
+    # replay + one pinned D2H read of losses/status + StepReport).  Every
+    # cfg.steps_per_frame steps -- the cadence at which run_mapping ingests a
+    # frame (trainer.py:554-561) -- a frame's map growth is applied through
+    # Mapper.add_keyframe: a new keyframe (crop from host memory) for 10% of
+    # the objects, rotating, so the crops go host -> device, the sampling
+    # tables are rebuilt and re-uploaded and the prefetched batch is redrawn.
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
-    h2d = d2h = 0
+    local = [mapper.instance_for_model(j) for j in range(k_local)]
+    n_new = max(1, k_local // 10)
+    frame_id = 10 ** 6
+    b0 = mapper.arena.uploaded_bytes
+    tables = 0
     t0 = time.perf_counter()
     for i in range(args.steps):
-        if i % cfg.steps_per_frame == 0:
-            mapper.invalidate()
+        if i % cfg.steps_per_frame == 0 and i > 0 and local:
+            frame_id += 1
+            for j in range(n_new):
+                inst = local[(frame_id * n_new + j) % len(local)]
+                kf = inst.keyframes[0]
+                mapper.add_keyframe(inst, frame_id, kf.pose, kf.bbox, kf.mask, scene["rgb"], scene["depth"])
         rep = mapper.train_step()
+        tables += mapper.last_io_bytes()[0] if (i % cfg.steps_per_frame == 0 and i > 0) else 0
         shard.gather_losses(rep)
     torch.cuda.synchronize()
     e2e_s = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
     if world > 1:
         torch.distributed.all_reduce(e2e_s, op=torch.distributed.ReduceOp.MAX)
     e2e_value = k_total * args.steps / float(e2e_s.item())
-    h2d, d2h = mapper.last_io_bytes()
-    h2d = -(-h2d // cfg.steps_per_frame)  # table upload amortised over the frame's steps
+    d2h = mapper.last_io_bytes()[1]
+    h2d = -(-(mapper.arena.uploaded_bytes - b0 + tables) // args.steps)  # crops + tables, per step
 
     # rooflines: algorithmic FLOPs per launch / CUDA-event duration of that
     # launch (same step, eager replay with L2 flushed).  KF (objects, FP32

@@ -25,6 +25,8 @@ class KeyframeArena:
         self.rgbd = torch.zeros((capacity_texels, 4), dtype=torch.float32, device=self.device)
         self.mask = torch.zeros(capacity_texels, dtype=torch.uint8, device=self.device)
         self.used = 0
+        self.uploaded_bytes = 0  # host->device crop bytes so far (texel float4 + mask byte)
+        self._pin_tex = self._pin_msk = self._pin_done = None
 
     def _reserve(self, n: int) -> None:
         need = self.used + n
@@ -56,8 +58,7 @@ class KeyframeArena:
             sizes.append(h * w)
         total = int(sum(sizes))
         self._reserve(total)
-        tex = np.empty((total, 4), np.float32)
-        msk = np.empty(total, np.uint8)
+        tex, msk = self._staging(total)
         off = 0
         for kf, n in zip(kfs, sizes):
             tex[off:off + n, :3] = kf.rgb.reshape(n, 3)
@@ -66,9 +67,32 @@ class KeyframeArena:
             kf.texel_off = self.used + off
             off += n
         base = self.used
-        self.rgbd[base:base + total] = torch.from_numpy(tex).to(self.device)
-        self.mask[base:base + total] = torch.from_numpy(msk).to(self.device)
+        if self._pin_tex is not None:  # pinned staging: asynchronous copies straight into the arena
+            self.rgbd[base:base + total].copy_(self._pin_tex[:total], non_blocking=True)
+            self.mask[base:base + total].copy_(self._pin_msk[:total], non_blocking=True)
+            self._pin_done = torch.cuda.Event()
+            self._pin_done.record()
+        else:
+            self.rgbd[base:base + total] = torch.from_numpy(tex).to(self.device)
+            self.mask[base:base + total] = torch.from_numpy(msk).to(self.device)
         self.used += total
+        self.uploaded_bytes += 17 * total
+
+    def _staging(self, n: int):
+        """Host arrays for n texels: views of a persistent pinned buffer on a
+        CUDA arena (waiting for the previous asynchronous copy out of it),
+        plain numpy otherwise."""
+        if self.device.type != "cuda":
+            self._pin_tex = None
+            return np.empty((n, 4), np.float32), np.empty(n, np.uint8)
+        if getattr(self, "_pin_tex", None) is None or self._pin_tex.shape[0] < n:
+            cap = max(1 << 16, 1 << (n - 1).bit_length())
+            self._pin_tex = torch.empty((cap, 4), dtype=torch.float32, pin_memory=True)
+            self._pin_msk = torch.empty(cap, dtype=torch.uint8, pin_memory=True)
+            self._pin_done = None
+        if getattr(self, "_pin_done", None) is not None:
+            self._pin_done.synchronize()
+        return self._pin_tex[:n].numpy(), self._pin_msk[:n].numpy()
 
     def add(self, kf) -> int:
         """Upload one Keyframe's crops; records kf.texel_off and returns it."""
@@ -85,6 +109,7 @@ class KeyframeArena:
         self.rgbd[off:off + n] = torch.from_numpy(tex).to(self.device)
         self.mask[off:off + n] = torch.from_numpy(kf.mask.reshape(n).astype(np.uint8)).to(self.device)
         self.used += n
+        self.uploaded_bytes += 17 * n
         kf.texel_off = off
         return off
 
@@ -128,7 +153,10 @@ class DeviceTable:
             return self.buf
         self.last = raw
         if self.buf is None or self.buf.numel() < n:
-            cap = max(256, 1 << (n - 1).bit_length())
+            # 2x headroom over the next power of two: a growing map (keyframes
+            # appended every few frames) reallocates -- and so re-captures the
+            # step graphs -- only O(log) times
+            cap = max(256, 2 << (n - 1).bit_length())
             self.buf = torch.zeros(cap, dtype=torch.uint8, device=self.device)
             self.pinned = torch.zeros(cap, dtype=torch.uint8, pin_memory=True)
             self.done = None

@@ -305,6 +305,10 @@ int vm_profile_read(int* launches, double* total_ms);   /* syncs on the events; 
 /* tag: 0 = MLP phase (fork .. join), 1 = FFMA kernel KF, 2 = tensor-core branch (KT + its partial reduce), 3 = Adam */
 int vm_profile_read_tag(int tag, int* launches, double* total_ms);
 int vm_profile_kernels(long* n);                        /* kernels launched since enable */
+/* VM_TRACE=1 in the environment: each vm_train_step records its FFMA work
+ * items (kind 1) and KT tiles (kind 2) as (kind, SM id, start ns, end ns);
+ * reads the last step's records (syncs the device). */
+int vm_trace_read(unsigned long long* out, int max_records, int* n_records);
 void vm_profile_count_kernels(int n);                   /* internal: launch counter */
 /* CTA count and dynamic smem the fused kernel would use for these stacks. */
 int vm_train_grid(const VmStack* stacks, const VmBatch* batches, int n_stacks, int* ctas, int* smem_bytes);

@@ -133,6 +133,7 @@ _SIGNATURES = {
     "vm_profile_read": (C.c_int, [C.POINTER(C.c_int), C.POINTER(C.c_double)]),
     "vm_profile_read_tag": (C.c_int, [C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_double)]),
     "vm_profile_kernels": (C.c_int, [C.POINTER(C.c_long)]),
+    "vm_trace_read": (C.c_int, [C.POINTER(C.c_ulonglong), C.c_int, C.POINTER(C.c_int)]),
     "vm_profile_count_kernels": (None, [C.c_int]),
     "vm_train_grid": (C.c_int, [C.POINTER(VmStack), C.POINTER(VmBatch), C.c_int, C.POINTER(C.c_int),
                                 C.POINTER(C.c_int)]),

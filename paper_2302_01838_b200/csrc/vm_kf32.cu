@@ -655,18 +655,22 @@ __device__ __forceinline__ void train_item(const KParams& p, int item, float* sm
 template <int SFIX>
 __global__ void __launch_bounds__(NTHR, 2) kf32_train_kernel(const __grid_constant__ KParams p) {
   extern __shared__ __align__(16) float smem[];
+  const unsigned long long t_start = p.trace ? vm_gtime() : 0;
   if (!p.queue) {
     train_item<SFIX>(p, blockIdx.x, smem);
+    if (p.trace && threadIdx.x == 0) vm_trace_rec(p.trace, 1, t_start);
     return;
   }
   __shared__ int s_item;
   for (;;) {
+    const unsigned long long t0 = p.trace ? vm_gtime() : 0;
     if (threadIdx.x == 0) s_item = atomicAdd(p.queue, 1);
     __syncthreads();
     const int item = s_item;
     if (item >= p.n_items) break;
     train_item<SFIX>(p, item, smem);
     __syncthreads();  // smem (weights, team regions, s_item) free for the next item
+    if (p.trace && threadIdx.x == 0) vm_trace_rec(p.trace, 1, t0);
   }
 }
 

@@ -863,6 +863,23 @@ extern "C" size_t vm_train_workspace_bytes(const VmStack* stacks, const VmBatch*
   return pl.ws_bytes;
 }
 
+// VM_TRACE=1: every vm_train_step records (kind 1 = FFMA item, 2 = KT tile,
+// SM id, start/end globaltimer ns) into a device buffer read by vm_trace_read.
+namespace {
+unsigned long long* g_trace = nullptr;
+unsigned long long* trace_buffer(cudaStream_t s) {
+  static const bool on = [] {
+    const char* e = std::getenv("VM_TRACE");
+    return e && e[0] == '1';
+  }();
+  if (!on) return nullptr;
+  if (!g_trace && cudaMalloc(&g_trace, sizeof(unsigned long long) * (1 + 4 * (1 << 16))) != cudaSuccess)
+    return nullptr;
+  cudaMemsetAsync(g_trace, 0, sizeof(unsigned long long), s);
+  return g_trace;
+}
+}  // namespace
+
 extern "C" int vm_train_step(const VmStack* stacks, const VmBatch* batches, int n_stacks, VmLossWeights w,
                              float* losses, int32_t* status, void* workspace, size_t workspace_bytes,
                              void* stream) {
@@ -910,6 +927,7 @@ extern "C" int vm_train_step(const VmStack* stacks, const VmBatch* batches, int 
     return !(e && e[0] == '0');
   }();
   if (kf_persist) kf.queue = reinterpret_cast<int*>(ws + pl.off_queue);
+  kf.trace = pl.kp.trace = trace_buffer(s);
   int ff_grid = 0;
   for (int i = 0; i < n_stacks; ++i) {
     if (pl.kp.s[i].tc) continue;
@@ -1137,6 +1155,21 @@ extern "C" int vm_backward(const VmStack* st, const float* encoded, int64_t n_sa
                            const float* grad_col, float* grads, void* stream) {
   return run_fwd_bwd(st, encoded, n_samples, grad_occ, grad_col, nullptr, nullptr, grads, true,
                      cudaStream_t(stream));
+}
+
+extern "C" int vm_trace_read(unsigned long long* out, int max_records, int* n_records) {
+  VM_REQUIRE(out && n_records, "vm_trace_read: null argument");
+  if (!g_trace) {
+    *n_records = 0;
+    return VM_OK;
+  }
+  VM_CUDA(cudaDeviceSynchronize());
+  unsigned long long n = 0;
+  VM_CUDA(cudaMemcpy(&n, g_trace, sizeof(n), cudaMemcpyDeviceToHost));
+  n = std::min<unsigned long long>(n, std::min(max_records, 1 << 16));
+  VM_CUDA(cudaMemcpy(out, g_trace + 1, sizeof(unsigned long long) * 4 * n, cudaMemcpyDeviceToHost));
+  *n_records = int(n);
+  return VM_OK;
 }
 
 extern "C" int vm_tc_debug_read(int* out) {

@@ -100,7 +100,30 @@ struct KParams {
   int n_stacks;
   int* queue;      // persistent FFMA kernel: next work item (zeroed before the launch), or null
   int n_items;     // work items over all stacks (persistent kernel)
+  unsigned long long* trace;  // VM_TRACE=1: per-CTA/item schedule records, or null
 };
+
+__device__ __forceinline__ unsigned long long vm_gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ unsigned vm_smid() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %smid;" : "=r"(r));
+  return r;
+}
+// one schedule record (kind, SM, start ns, end ns); called by one thread
+__device__ __forceinline__ void vm_trace_rec(unsigned long long* tr, int kind, unsigned long long t0) {
+  if (!tr) return;
+  const unsigned slot = atomicAdd(reinterpret_cast<unsigned*>(tr), 1u);
+  if (slot >= (1u << 16)) return;
+  unsigned long long* r = tr + 1 + 4ull * slot;
+  r[0] = kind;
+  r[1] = vm_smid();
+  r[2] = t0;
+  r[3] = vm_gtime();
+}
 
 // vm_kf32.cu: the specialised hidden-32 / 4-layer train kernel
 bool kf32_supported(const KParams& p);

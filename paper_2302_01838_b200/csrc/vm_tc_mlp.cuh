@@ -281,6 +281,7 @@ __global__ void __launch_bounds__(kTCThreads, 1)
   using SM = Smem<H, L>;
   extern __shared__ __align__(1024) uint8_t smem[];
   const KStack& st = p.s[si];
+  const unsigned long long t_start = p.trace ? vm_gtime() : 0;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int k = blockIdx.x / st.P, tile = blockIdx.x % st.P;
   const int S = st.S, G = kTM / S;
@@ -840,6 +841,7 @@ __global__ void __launch_bounds__(kTCThreads, 1)
   tc::fence_before_sync();
   __syncthreads();
   if (warp == 0) tc::tmem_free(tm, 512);
+  if (p.trace && tid == 0) vm_trace_rec(p.trace, 2, t_start);
   if (st.P > 1) return;
   // single-tile model: finish like KF's P == 1 path
   __threadfence_block();

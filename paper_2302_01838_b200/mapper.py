@@ -369,6 +369,7 @@ class Mapper:
         host_s = torch.empty(4 * len(stacks(0)), dtype=torch.int32, pin_memory=True)
         side = torch.cuda.Stream(dev)
         side_bg = torch.cuda.Stream(dev)
+        sample_first = os.environ.get("VM_SAMPLE_FIRST", "0") == "1"  # A/B: capture the sampler first
         graphs = []
         for p in (0, 1):
             g = torch.cuda.CUDAGraph()
@@ -384,11 +385,21 @@ class Mapper:
                     # step t's training
                     side.wait_stream(cur)
                     side_bg.wait_stream(cur)
-                    with torch.cuda.stream(side):
-                        sample_obj(1 - p, 1)
-                    with torch.cuda.stream(side_bg):
-                        sample_bg(1 - p, 1)
+                    if sample_first:
+                        with torch.cuda.stream(side):
+                            sample_obj(1 - p, 1)
+                        with torch.cuda.stream(side_bg):
+                            sample_bg(1 - p, 1)
                     losses, status = launch_train(stacks(p), c.loss_weights, self._ws, bump_version=False)
+                    if not sample_first:
+                        # captured after the training kernels (they still do not
+                        # depend on each other), so the graph launches the
+                        # training grids first and the sampler's many small CTAs
+                        # fill in behind them instead of delaying them
+                        with torch.cuda.stream(side):
+                            sample_obj(1 - p, 1)
+                        with torch.cuda.stream(side_bg):
+                            sample_bg(1 - p, 1)
                     host_l.copy_(losses, non_blocking=True)
                     host_s.copy_(status, non_blocking=True)
                     cur.wait_stream(side)

@@ -65,6 +65,31 @@ inline int compute_layout(const VmArch& a, VmLayout& L) {
   return VM_OK;
 }
 
+// ---------------------------------------------------------------- schedule tracing (VM_TRACE=1)
+unsigned long long* trace_ptr();  // host: VM_TRACE buffer or null (vm_mlp.cu)
+
+__device__ __forceinline__ unsigned long long vm_gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ unsigned vm_smid() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %smid;" : "=r"(r));
+  return r;
+}
+// one schedule record (kind, SM, start ns, end ns); called by one thread
+__device__ __forceinline__ void vm_trace_rec(unsigned long long* tr, int kind, unsigned long long t0) {
+  if (!tr) return;
+  const unsigned slot = atomicAdd(reinterpret_cast<unsigned*>(tr), 1u);
+  if (slot >= (1u << 16)) return;
+  unsigned long long* r = tr + 1 + 4ull * slot;
+  r[0] = kind;
+  r[1] = vm_smid();
+  r[2] = t0;
+  r[3] = vm_gtime();
+}
+
 // ---------------------------------------------------------------- device
 __device__ __forceinline__ float4 ld4(const float* p) { return *reinterpret_cast<const float4*>(p); }
 __device__ __forceinline__ void st4(float* p, float4 v) { *reinterpret_cast<float4*>(p) = v; }
@@ -140,7 +165,7 @@ __device__ float pairwise_sum(const F& get, int64_t n) {
 // elements, in depth-first order; returns their count (only the first
 // max_leaves are stored).  Lets a CTA sum the leaves in parallel and combine
 // them with pairwise_combine in exactly the recursive order.
-__device__ inline int pairwise_leaves(int64_t n, int64_t* start, int* len, int max_leaves) {
+__host__ __device__ inline int pairwise_leaves(int64_t n, int64_t* start, int* len, int max_leaves) {
   int64_t si[24], sn[24];  // depth <= log2(n / 128) + 1 <= 24 for any int32 row count
   int sp = 0, cnt = 0;
   si[sp] = 0;

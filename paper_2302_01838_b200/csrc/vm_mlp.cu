@@ -98,6 +98,13 @@ __host__ __device__ inline int red_chunk_floats(int P) { return P <= kRedDirect 
 
 __global__ void __launch_bounds__(kRedThreads, 6) reduce_partials_kernel(const __grid_constant__ KParams p,
                                                                           int only_stack) {
+  struct Rec {  // schedule record at every exit
+    const KParams& p;
+    unsigned long long t;
+    __device__ ~Rec() {
+      if (p.trace && threadIdx.x == 0) vm_trace_rec(p.trace, 3, t);
+    }
+  } rec{p, p.trace ? vm_gtime() : 0ull};
   extern __shared__ __align__(16) float red_smem[];
   __shared__ float4 gsum[kRedGroups][kRedChunk / 4];
   int b = blockIdx.x, si = 0;
@@ -134,7 +141,7 @@ __global__ void __launch_bounds__(kRedThreads, 6) reduce_partials_kernel(const _
       finite = isfinite(tot.x) && isfinite(tot.y) && isfinite(tot.z) && isfinite(tot.w);
     }
     const bool all_finite = __syncthreads_and(finite);
-    finalize_model(st, k, all_finite, ch == 0, red_smem, st.R * 3);
+    finalize_model(st, k, all_finite, ch == 0, red_smem, st.R * 3, !st.ls_sep);
     return;
   }
   const int col = threadIdx.x % (kRedChunk / 4), q = threadIdx.x / (kRedChunk / 4);
@@ -174,7 +181,52 @@ __global__ void __launch_bounds__(kRedThreads, 6) reduce_partials_kernel(const _
     finite = isfinite(tot.x) && isfinite(tot.y) && isfinite(tot.z) && isfinite(tot.w);
   }
   const bool all_finite = __syncthreads_and(finite);
-  finalize_model(st, k, all_finite, ch == 0, red_smem, st.R * 3);
+  finalize_model(st, k, all_finite, ch == 0, red_smem, st.R * 3, !st.ls_sep);
+}
+
+// Pairwise-summation leaves of an R-row column (host-computed once per call).
+struct LeafTable {
+  int n;
+  int start[64], len[64];
+};
+
+// Loss sums of a tensor-core stack's models: one CTA per (model, loss term):
+// the column is staged in smem, each leaf of numpy's pairwise recursion is
+// summed by its own thread, and thread 0 combines the leaves in the
+// recursion's order (same bits as pairwise_sum over the column).  Runs on a
+// second branch concurrently with the partial reduce and Adam.
+__global__ void __launch_bounds__(128) loss_sums_kernel(const __grid_constant__ KParams p, int si,
+                                                        const __grid_constant__ LeafTable lt) {
+  extern __shared__ __align__(16) float ls_col[];
+  __shared__ float lf_sum[64];
+  const unsigned long long t0 = p.trace ? vm_gtime() : 0;
+  const KStack& st = p.s[si];
+  const int k = blockIdx.x, j = blockIdx.y, tid = threadIdx.x, R = st.R;
+  const float* terms = st.ray_terms + int64_t(k) * R * 3;
+  const int live = st.model_rays ? min(st.model_rays[k], R) : R;  // padding rows sum as 0 (config 3)
+  for (int r0 = 0; r0 < R; r0 += 8 * 128) {
+    float v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int r = r0 + u * 128 + tid;
+      v[u] = r < live ? __ldcg(terms + int64_t(r) * 3 + j) : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int r = r0 + u * 128 + tid;
+      if (r < R) ls_col[r] = v[u];
+    }
+  }
+  __syncthreads();
+  if (tid < lt.n) lf_sum[tid] = pairwise_sum_leaf([&](int64_t r) { return ls_col[r]; }, lt.start[tid], lt.len[tid]);
+  __syncthreads();
+  if (tid == 0) {
+    int next = 0;
+    const float sum = pairwise_combine(R, lf_sum, next);
+    st.losses[int64_t(k) * 3 + j] = sum;
+    if (!isfinite(sum)) atomicMin(&st.status[1], k);
+    if (p.trace) vm_trace_rec(p.trace, 7, t0);
+  }
 }
 
 template <int H, int L, int MODE>
@@ -505,9 +557,18 @@ struct AdamStack {
 struct AdamParams {
   AdamStack s[2];
   int n_stacks;
+  unsigned long long* trace;
 };
 
 __global__ void __launch_bounds__(256) adam_train_kernel(const __grid_constant__ AdamParams p, int block_offset) {
+  const unsigned long long t_start = p.trace ? vm_gtime() : 0;
+  struct Rec {  // schedule record at every exit
+    const AdamParams& p;
+    unsigned long long t;
+    __device__ ~Rec() {
+      if (p.trace && threadIdx.x == 0) vm_trace_rec(p.trace, 4, t);
+    }
+  } rec{p, t_start};
   int b = blockIdx.x + block_offset, si = 0;
   if (p.n_stacks > 1 && b >= p.s[1].item_base) si = 1;
   const AdamStack& s = p.s[si];
@@ -765,6 +826,11 @@ int plan_train(const VmStack* stacks, const VmBatch* batches, int n, TrainPlan& 
     ks.n_items = ks.items ? b.n_work_items : 0;
     VM_REQUIRE(!ks.items || ks.n_items >= 0, "vm_train_step: bad work-item count");
     ks.tc = tc_enabled() && ks.H == 128 && ks.L == 4 && ks.D <= tck::kK0 && ks.S <= 32 ? 1 : 0;
+    {
+      int64_t st64[64];
+      int len[64];
+      ks.ls_sep = ks.tc && pairwise_leaves(ks.R, st64, len, 64) <= 64 ? 1 : 0;
+    }
   }
   choose_splits(pl.kp.s, n, P);
   for (int i = 0; i < n; ++i) {
@@ -867,17 +933,25 @@ extern "C" size_t vm_train_workspace_bytes(const VmStack* stacks, const VmBatch*
 // SM id, start/end globaltimer ns) into a device buffer read by vm_trace_read.
 namespace {
 unsigned long long* g_trace = nullptr;
-unsigned long long* trace_buffer(cudaStream_t s) {
+}  // namespace
+
+// The trace buffer (allocated on first use when VM_TRACE=1, else null); the
+// record counter is reset by vm_trace_read, so a read returns every record
+// since the previous one (e.g. one replayed step graph, sampler included).
+unsigned long long* vm::trace_ptr() {
   static const bool on = [] {
     const char* e = std::getenv("VM_TRACE");
     return e && e[0] == '1';
   }();
   if (!on) return nullptr;
-  if (!g_trace && cudaMalloc(&g_trace, sizeof(unsigned long long) * (1 + 4 * (1 << 16))) != cudaSuccess)
-    return nullptr;
-  cudaMemsetAsync(g_trace, 0, sizeof(unsigned long long), s);
+  if (!g_trace) {
+    if (cudaMalloc(&g_trace, sizeof(unsigned long long) * (1 + 4 * (1 << 16))) != cudaSuccess) return nullptr;
+    cudaMemset(g_trace, 0, sizeof(unsigned long long));
+  }
   return g_trace;
 }
+namespace {
+unsigned long long* trace_buffer(cudaStream_t) { return vm::trace_ptr(); }
 }  // namespace
 
 extern "C" int vm_train_step(const VmStack* stacks, const VmBatch* batches, int n_stacks, VmLossWeights w,
@@ -927,7 +1001,7 @@ extern "C" int vm_train_step(const VmStack* stacks, const VmBatch* batches, int 
     return !(e && e[0] == '0');
   }();
   if (kf_persist) kf.queue = reinterpret_cast<int*>(ws + pl.off_queue);
-  kf.trace = pl.kp.trace = trace_buffer(s);
+  kf.trace = pl.kp.trace = pl.ap.trace = trace_buffer(s);
   int ff_grid = 0;
   for (int i = 0; i < n_stacks; ++i) {
     if (pl.kp.s[i].tc) continue;
@@ -975,7 +1049,8 @@ extern "C" int vm_train_step(const VmStack* stacks, const VmBatch* batches, int 
   // concurrent callers on different threads or devices never share them
   struct SideRes {
     cudaStream_t side = nullptr;
-    cudaEvent_t fork = nullptr, join = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr, kt_done = nullptr, ls_done = nullptr;
+    cudaStream_t side2 = nullptr;  // loss sums of the tensor-core stacks
   };
   static thread_local SideRes side_res[64];
   int dev = 0;
@@ -984,6 +1059,9 @@ extern "C" int vm_train_step(const VmStack* stacks, const VmBatch* batches, int 
   cudaStream_t& side = side_res[dev].side;
   cudaEvent_t& ev_fork = side_res[dev].fork;
   cudaEvent_t& ev_join = side_res[dev].join;
+  cudaEvent_t& ev_kt = side_res[dev].kt_done;
+  cudaEvent_t& ev_ls = side_res[dev].ls_done;
+  cudaStream_t& side2 = side_res[dev].side2;
   bool forked = false;
   cudaStream_t ts = s;
   using TI = tck::Img<128, 4>;
@@ -1045,12 +1123,19 @@ extern "C" int vm_train_step(const VmStack* stacks, const VmBatch* batches, int 
       return e && e[0] == '1';
     }();
     if (!forked && (fn || use_kf32) && !no_fork) {
-      if (!side) {  // first use may be inside a graph capture: relax the capture mode for the creation
+      if (!side || !ev_kt) {  // first use may be inside a graph capture: relax the capture mode for the creation
         cudaStreamCaptureMode mode = cudaStreamCaptureModeRelaxed;
         VM_CUDA(cudaThreadExchangeStreamCaptureMode(&mode));
-        VM_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
-        VM_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
-        VM_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+        if (!side) {
+          VM_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+          VM_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+          VM_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+        }
+        if (!ev_kt) {
+          VM_CUDA(cudaEventCreateWithFlags(&ev_kt, cudaEventDisableTiming));
+          VM_CUDA(cudaEventCreateWithFlags(&ev_ls, cudaEventDisableTiming));
+          VM_CUDA(cudaStreamCreateWithFlags(&side2, cudaStreamNonBlocking));
+        }
         VM_CUDA(cudaThreadExchangeStreamCaptureMode(&mode));
       }
       VM_CUDA(cudaEventRecord(ev_fork, s));
@@ -1077,8 +1162,33 @@ extern "C" int vm_train_step(const VmStack* stacks, const VmBatch* batches, int 
     tck::tc_train_kernel<128, 4><<<ks.K * ks.P, tck::kTCThreads, smem_tc, ts>>>(pl.kp, i, img);
     VM_CUDA(cudaGetLastError());
     if (g_prof.on) g_prof.kernels += 1;
+    if (forked && ks.P > 1) VM_CUDA(cudaEventRecord(ev_kt, ts));
     rc = launch_reduce(pl, i, ts);
     if (rc) return rc;
+  }
+  // loss sums of the split tensor-core models: on a second branch once KT is
+  // done, concurrently with their partial reduce and Adam (only the host
+  // report needs them; Adam needs the reduce); joined after Adam
+  bool ls_forked = false;
+  for (int i = 0; i < n_stacks; ++i) {
+    const KStack& ks = pl.kp.s[i];
+    if (!ks.ls_sep || ks.K == 0 || ks.P <= 1) continue;
+    cudaStream_t ls = s;
+    if (forked) {
+      VM_CUDA(cudaStreamWaitEvent(side2, ev_kt, 0));
+      ls = side2;
+      ls_forked = true;
+    }
+    LeafTable lt;
+    int64_t st64[64];
+    lt.n = pairwise_leaves(ks.R, st64, lt.len, 64);  // <= 64: ls_sep
+    for (int l = 0; l < lt.n; ++l) lt.start[l] = int(st64[l]);
+    const int ls_smem = ks.R * 4;
+    if (ls_smem > 48 * 1024)
+      VM_CUDA(cudaFuncSetAttribute(loss_sums_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, ls_smem));
+    loss_sums_kernel<<<dim3(ks.K, 3), 128, ls_smem, ls>>>(pl.kp, i, lt);
+    VM_CUDA(cudaGetLastError());
+    if (g_prof.on) g_prof.kernels += 1;
   }
   if (kt1) VM_CUDA(cudaEventRecord(kt1, ts));
   if (!kf_done) {
@@ -1097,6 +1207,10 @@ extern "C" int vm_train_step(const VmStack* stacks, const VmBatch* batches, int 
   }
   rc = launch_adam(pl, s, adam_split);
   if (rc) return rc;
+  if (ls_forked) {
+    VM_CUDA(cudaEventRecord(ev_ls, side2));
+    VM_CUDA(cudaStreamWaitEvent(s, ev_ls, 0));
+  }
   if (r1) VM_CUDA(cudaEventRecord(r1, s));
   return VM_OK;
 }
@@ -1168,6 +1282,7 @@ extern "C" int vm_trace_read(unsigned long long* out, int max_records, int* n_re
   VM_CUDA(cudaMemcpy(&n, g_trace, sizeof(n), cudaMemcpyDeviceToHost));
   n = std::min<unsigned long long>(n, std::min(max_records, 1 << 16));
   VM_CUDA(cudaMemcpy(out, g_trace + 1, sizeof(unsigned long long) * 4 * n, cudaMemcpyDeviceToHost));
+  VM_CUDA(cudaMemset(g_trace, 0, sizeof(unsigned long long)));
   *n_records = int(n);
   return VM_OK;
 }

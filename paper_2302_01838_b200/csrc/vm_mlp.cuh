@@ -56,6 +56,7 @@ struct KStack {
   int w_off[VM_MAX_LAYERS], b_off[VM_MAX_LAYERS];
   int K, R, S, G, P;          // models, rays, points/ray, rays/block, CTAs per model
   int tc;                     // 1: trained by the tensor-core kernel KT (vm_tc_mlp.cuh)
+  int ls_sep;                 // 1: loss sums by loss_sums_kernel (split tensor-core stacks), not the reduce
   int64_t N;                  // samples per model (forward/backward modes)
   int model_base;             // global model index of model 0 (losses/status)
   int chunk;                  // ray blocks per work item (FFMA kernels)
@@ -103,27 +104,7 @@ struct KParams {
   unsigned long long* trace;  // VM_TRACE=1: per-CTA/item schedule records, or null
 };
 
-__device__ __forceinline__ unsigned long long vm_gtime() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
-__device__ __forceinline__ unsigned vm_smid() {
-  unsigned r;
-  asm volatile("mov.u32 %0, %smid;" : "=r"(r));
-  return r;
-}
-// one schedule record (kind, SM, start ns, end ns); called by one thread
-__device__ __forceinline__ void vm_trace_rec(unsigned long long* tr, int kind, unsigned long long t0) {
-  if (!tr) return;
-  const unsigned slot = atomicAdd(reinterpret_cast<unsigned*>(tr), 1u);
-  if (slot >= (1u << 16)) return;
-  unsigned long long* r = tr + 1 + 4ull * slot;
-  r[0] = kind;
-  r[1] = vm_smid();
-  r[2] = t0;
-  r[3] = vm_gtime();
-}
+
 
 // vm_kf32.cu: the specialised hidden-32 / 4-layer train kernel
 bool kf32_supported(const KParams& p);
@@ -349,8 +330,10 @@ struct WarpGrads {
 // non-finite flags Adam and the host need (models.py:423-428,
 // trainer.py:404-407); this step's bias corrections.  Called by all threads
 // of a CTA.  `meta` selects the writer of the per-model words.
+static __device__ __noinline__ void model_loss_sums(const KStack& st, int k, float* scratch, int scratch_floats);
+
 __device__ inline void finalize_model(const KStack& st, int k, bool all_finite, bool meta, float* scratch,
-                               int scratch_floats) {
+                               int scratch_floats, bool sums = true) {
   const int tid = threadIdx.x;
   // non-meta CTAs only need the update mask when their chunk is non-finite
   // (both conditions are CTA-uniform, so the barrier below is too)
@@ -361,6 +344,17 @@ __device__ inline void finalize_model(const KStack& st, int k, bool all_finite, 
   const bool active = upd && !st.frozen[k];
   if (tid == 0 && active && !all_finite) atomicMin(&st.status[0], k);
   if (!meta) return;
+  if (tid == 0) {
+    st.upd[k] = active ? 1 : 0;
+    st.corr[k] = bias_corrections(st.corr1, st.corr2, st.corr_len, st.beta1, st.beta2, st.step[k]);
+  }
+  if (sums) model_loss_sums(st, k, scratch, scratch_floats);
+}
+
+// The model's three loss sums over its rays in numpy's pairwise order
+// (render.py:301-308) and the non-finite-loss flag.  Called by all threads.
+static __device__ __noinline__ void model_loss_sums(const KStack& st, int k, float* scratch, int scratch_floats) {
+  const int tid = threadIdx.x;
   // stage the per-ray terms in smem (coalesced), then 3 threads sum them in
   // numpy's pairwise order without a global-load latency per add
   const float* terms = st.ray_terms + int64_t(k) * st.R * 3;
@@ -370,7 +364,22 @@ __device__ inline void finalize_model(const KStack& st, int k, bool all_finite, 
   const int live3 = 3 * (st.model_rays ? min(st.model_rays[k], st.R) : st.R);
   const bool staged = st.R * 3 <= scratch_floats;
   if (staged) {
-    for (int i = tid; i < st.R * 3; i += blockDim.x) scratch[i] = i < live3 ? __ldcg(terms + i) : 0.f;
+    // 8 independent loads in flight per thread (one L2 round trip per 8 rows
+    // of the CTA, not per row)
+    const int n3 = st.R * 3, nt = blockDim.x;
+    for (int i0 = 0; i0 < n3; i0 += 8 * nt) {
+      float v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int i = i0 + u * nt + tid;
+        v[u] = i < live3 ? __ldcg(terms + i) : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int i = i0 + u * nt + tid;
+        if (i < n3) scratch[i] = v[u];
+      }
+    }
     __syncthreads();
   }
   // more than one pairwise leaf: the leaves (<= 128 rays each) are summed by
@@ -404,10 +413,6 @@ __device__ inline void finalize_model(const KStack& st, int k, bool all_finite, 
                                             st.R);
     st.losses[int64_t(k) * 3 + j] = sum;
     if (!isfinite(sum)) atomicMin(&st.status[1], k);
-  }
-  if (tid == 0) {
-    st.upd[k] = active ? 1 : 0;
-    st.corr[k] = bias_corrections(st.corr1, st.corr2, st.corr_len, st.beta1, st.beta2, st.step[k]);
   }
 }
 

@@ -227,6 +227,18 @@ struct KS {
   int64_t* aux_u;
   int64_t* aux_v;
   double* aux_t64;
+  unsigned long long* trace;  // VM_TRACE schedule records, or null
+};
+
+// schedule record of one CTA at every exit of a sampler kernel
+struct TraceOnExit {
+  unsigned long long* tr;
+  int kind;
+  unsigned long long t;
+  __device__ TraceOnExit(unsigned long long* tr_, int kind_) : tr(tr_), kind(kind_), t(tr_ ? vm_gtime() : 0) {}
+  __device__ ~TraceOnExit() {
+    if (tr && threadIdx.x == 0) vm_trace_rec(tr, kind, t);
+  }
 };
 
 // Block-wide exclusive scan of one int per thread (blockDim.x == 256).
@@ -265,6 +277,7 @@ __device__ __forceinline__ int object_rays(const VmSampleObject& ob, const VmSam
 
 // ---- per object: stream seeds, keyframe index per ray, normal resolution.
 __global__ void __launch_bounds__(kST) sample_prep_kernel(const __grid_constant__ KS ks) {
+  TraceOnExit rec(ks.trace, 5);
   extern __shared__ __align__(16) unsigned char sm[];
   __shared__ uint64_t s_ki[256];
   __shared__ double s_wi[256], s_fi[256];
@@ -486,6 +499,7 @@ __global__ void __launch_bounds__(kST) sample_prep_kernel(const __grid_constant_
 
 // ---- per ray: pixel, gathers, f64 geometry, depth-guided samples, outputs.
 __global__ void __launch_bounds__(kRT) sample_rays_kernel(const __grid_constant__ KS ks, int n_objects) {
+  TraceOnExit rec(ks.trace, 6);
   const VmSampleParams& P = ks.p;
   const int R = P.n_rays, S = ks.S, nc = P.n_stratified, nsf = P.n_surface;
   const int64_t rg = blockIdx.x * int64_t(kRT) + threadIdx.x;
@@ -786,6 +800,7 @@ extern "C" int vm_sample(const VmSampleObject* objects, int n_objects, const VmK
   ks.bases = reinterpret_cast<int64_t*>(ws + pl.off_bases);
   ks.nrm = reinterpret_cast<double*>(ws + pl.off_nrm);
   ks.status = reinterpret_cast<int*>(ws + pl.off_status);
+  ks.trace = trace_ptr();
   if (aux) {
     ks.aux_kf = aux->kf_idx;
     ks.aux_u = aux->u;

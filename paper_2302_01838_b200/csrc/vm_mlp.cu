@@ -105,6 +105,9 @@ __global__ void __launch_bounds__(kRedThreads, 6) reduce_partials_kernel(const _
       if (p.trace && threadIdx.x == 0) vm_trace_rec(p.trace, 3, t);
     }
   } rec{p, p.trace ? vm_gtime() : 0ull};
+  // launched with programmatic stream serialization behind KT: the CTAs may
+  // be resident before KT finishes and wait here for its partials
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   extern __shared__ __align__(16) float red_smem[];
   __shared__ float4 gsum[kRedGroups][kRedChunk / 4];
   int b = blockIdx.x, si = 0;
@@ -868,6 +871,15 @@ int plan_train(const VmStack* stacks, const VmBatch* batches, int n, TrainPlan& 
   pl.ws_bytes = off;
   return VM_OK;
 }
+// VM_PDL=0 disables programmatic dependent launch (A/B).
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("VM_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 // Partial reduce of a tensor-core stack (its tiles' weight-gradient blocks;
 // FFMA stacks reduce in-kernel).  Runs on the tensor-core branch's stream so
 // it overlaps the FFMA kernel.
@@ -880,8 +892,20 @@ int launch_reduce(const TrainPlan& pl, int i, cudaStream_t s) {
     const int red_smem = ks.R * 3 * 4;
     if (red_smem > 48 * 1024)
       VM_CUDA(cudaFuncSetAttribute(reduce_partials_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, red_smem));
-    reduce_partials_kernel<<<grid, kRedThreads, red_smem, s>>>(pl.kp, i);
-    VM_CUDA(cudaGetLastError());
+    // programmatic dependent launch (Blackwell/Hopper): the reduce grid is
+    // scheduled while KT drains and released by griddepcontrol.wait, hiding
+    // the launch gap on the step's critical path
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kRedThreads);
+    cfg.dynamicSmemBytes = red_smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    VM_CUDA(cudaLaunchKernelEx(&cfg, reduce_partials_kernel, pl.kp, i));
     if (g_prof.on) g_prof.kernels += 1;
   }
   return VM_OK;

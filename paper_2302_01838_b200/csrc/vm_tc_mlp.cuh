@@ -756,6 +756,10 @@ __global__ void __launch_bounds__(kTCThreads, 1)
             myDb[l * H + c0 + 32 * g + lane] += warp_colsum(v);
           }
           if (l == 0) {
+            // last weight-gradient GEMM of the tile: let the partial-reduce
+            // grid (launched programmatically behind this one) be scheduled
+            // now; it waits on griddepcontrol.wait for this grid's completion
+            asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
             // layer-0 input recomputed (positional encoding), features
             // 40..127 are zero padding so M = 128
             float xa[32], xb[32];

@@ -699,8 +699,7 @@ int launch_kf32(const KParams& p, int grid, cudaStream_t s) {
     static int sms = 0;
     if (!sms) VM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
     q.n_items = grid;
-    grid = std::min(grid, 2 * sms);
-    VM_CUDA(cudaMemsetAsync(q.queue, 0, sizeof(int), s));
+    grid = std::min(grid, 2 * sms);  // the counter was zeroed by vm_train_step's init kernel
   }
   void* args[] = {&q};
   VM_CUDA(cudaLaunchKernel(fn, dim3(grid), dim3(kf32::NTHR), args, smem, s));

@@ -871,6 +871,20 @@ int plan_train(const VmStack* stacks, const VmBatch* batches, int n, TrainPlan& 
   pl.ws_bytes = off;
   return VM_OK;
 }
+struct StepInit {
+  int32_t* status;
+  int n_status;
+  int* cnt[2];
+  int n_cnt[2];
+  int* queue;
+};
+__global__ void step_init_kernel(const __grid_constant__ StepInit in) {
+  for (int i = threadIdx.x; i < in.n_status; i += blockDim.x) in.status[i] = 0x7f7f7f7f;
+  for (int j = 0; j < 2; ++j)
+    for (int i = threadIdx.x; i < in.n_cnt[j]; i += blockDim.x) in.cnt[j][i] = 0;
+  if (threadIdx.x == 0) *in.queue = 0;
+}
+
 // VM_PDL=0 disables programmatic dependent launch (A/B).
 bool pdl_enabled() {
   static const bool on = [] {
@@ -987,12 +1001,24 @@ extern "C" int vm_train_step(const VmStack* stacks, const VmBatch* batches, int 
   VM_REQUIRE(workspace_bytes >= pl.ws_bytes, "vm_train_step: workspace too small");
   cudaStream_t s = cudaStream_t(stream);
   char* ws = static_cast<char*>(workspace);
-  VM_CUDA(cudaMemsetAsync(status, 0x7f, sizeof(int32_t) * 4 * n_stacks, s));
-  // chunk tickets of the in-kernel partial reduction (the workspace may have
-  // held another plan's data)
-  for (int i = 0; i < n_stacks; ++i)
-    if (!pl.kp.s[i].tc && pl.kp.s[i].P > 1 && pl.kp.s[i].K > 0)
-      VM_CUDA(cudaMemsetAsync(ws + pl.off_cnt[i], 0, sizeof(int) * pl.kp.s[i].K, s));
+  // one init kernel: status words to the "no failure" pattern, the chunk
+  // tickets of the in-kernel partial reductions (the workspace may have held
+  // another plan's data) and the persistent kernel's item counter
+  {
+    StepInit in;
+    std::memset(&in, 0, sizeof(in));
+    in.status = status;
+    in.n_status = 4 * n_stacks;
+    for (int i = 0; i < n_stacks; ++i)
+      if (!pl.kp.s[i].tc && pl.kp.s[i].K > 0) {
+        in.cnt[i] = reinterpret_cast<int*>(ws + pl.off_cnt[i]);
+        in.n_cnt[i] = pl.kp.s[i].K;
+      }
+    in.queue = reinterpret_cast<int*>(ws + pl.off_queue);
+    step_init_kernel<<<1, 256, 0, s>>>(in);
+    VM_CUDA(cudaGetLastError());
+    if (g_prof.on) g_prof.kernels += 1;
+  }
   int loss_off = 0;
   for (int i = 0; i < n_stacks; ++i) {
     KStack& ks = pl.kp.s[i];

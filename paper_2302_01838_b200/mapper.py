@@ -365,8 +365,10 @@ class Mapper:
         launch_train(stacks(0), c.loss_weights, self._ws, bump_version=False)  # state restored by caller
         torch.cuda.synchronize(dev)
         n = sum(p.count for p, _, _ in stacks(0))
-        host_l = torch.empty((n, 3), dtype=torch.float32, pin_memory=True)
-        host_s = torch.empty(4 * len(stacks(0)), dtype=torch.int32, pin_memory=True)
+        n_st = len(stacks(0))
+        host_io = torch.empty(3 * max(n, 1) + 4 * n_st, dtype=torch.int32, pin_memory=True)
+        host_l = host_io[:3 * max(n, 1)].view(torch.float32).view(max(n, 1), 3)[:n]
+        host_s = host_io[3 * max(n, 1):]
         side = torch.cuda.Stream(dev)
         side_bg = torch.cuda.Stream(dev)
         sample_first = os.environ.get("VM_SAMPLE_FIRST", "0") == "1"  # A/B: capture the sampler first
@@ -400,8 +402,7 @@ class Mapper:
                             sample_obj(1 - p, 1)
                         with torch.cuda.stream(side_bg):
                             sample_bg(1 - p, 1)
-                    host_l.copy_(losses, non_blocking=True)
-                    host_s.copy_(status, non_blocking=True)
+                    host_io.copy_(self._ws.results(n, n_st), non_blocking=True)  # losses + status, one copy
                     cur.wait_stream(side)
                     cur.wait_stream(side_bg)
                     _lib.check(_lib.load().vm_step_advance(step_dev.data_ptr(), 1, _lib.stream_ptr()),

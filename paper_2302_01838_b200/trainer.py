@@ -115,16 +115,23 @@ class TrainWorkspace:
 
     def __init__(self):
         self.ws = None
+        self.io = None       # int32: losses [K, 3] (f32 bits) then status [4 * stacks], contiguous
         self.losses = None
         self.status = None
 
     def ensure(self, nbytes: int, n_models: int, n_stacks: int, device) -> None:
         if self.ws is None or self.ws.numel() < nbytes:
             self.ws = torch.zeros(max(nbytes, 256), dtype=torch.uint8, device=device)
-        if self.losses is None or self.losses.shape[0] < n_models:
-            self.losses = torch.zeros((max(n_models, 1), 3), dtype=torch.float32, device=device)
-        if self.status is None or self.status.numel() < 4 * n_stacks:
-            self.status = torch.zeros(4 * max(n_stacks, 2), dtype=torch.int32, device=device)
+        need = 3 * max(n_models, 1) + 4 * max(n_stacks, 2)
+        if self.io is None or self.io.numel() < need:
+            self.io = torch.zeros(2 * need, dtype=torch.int32, device=device)
+        # status right behind this call's losses: one device->host copy reads both
+        self.losses = self.io[:3 * max(n_models, 1)].view(torch.float32).view(max(n_models, 1), 3)
+        self.status = self.io[3 * max(n_models, 1):3 * max(n_models, 1) + 4 * max(n_stacks, 2)]
+
+    def results(self, n_models: int, n_stacks: int) -> torch.Tensor:
+        """The contiguous int32 view [losses (3 n_models) | status (4 n_stacks)]."""
+        return self.io[:3 * max(n_models, 1) + 4 * n_stacks]
 
 
 _default_ws = TrainWorkspace()

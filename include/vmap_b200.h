@@ -315,6 +315,11 @@ int vm_train_grid(const VmStack* stacks, const VmBatch* batches, int n_stacks, i
 
 /* Device step counter used by graph-replayed steps: *counter += inc. */
 int vm_step_advance(int64_t* counter, int64_t inc, void* stream);
+/* End of a captured step: copy n_words result words (losses + status) into
+ * pinned host memory by device stores (no copy-engine transfer) and advance
+ * the device step counter by inc. */
+int vm_step_finish(const int32_t* words, int32_t* host_words, int32_t n_words, int64_t* counter, int64_t inc,
+                   void* stream);
 
 /* ---- misc ---------------------------------------------------------------- */
 const char* vm_last_error(void);

@@ -877,12 +877,17 @@ struct StepInit {
   int* cnt[2];
   int n_cnt[2];
   int* queue;
+  unsigned long long* trace;
 };
 __global__ void step_init_kernel(const __grid_constant__ StepInit in) {
+  const unsigned long long t0 = in.trace ? vm_gtime() : 0;
   for (int i = threadIdx.x; i < in.n_status; i += blockDim.x) in.status[i] = 0x7f7f7f7f;
   for (int j = 0; j < 2; ++j)
     for (int i = threadIdx.x; i < in.n_cnt[j]; i += blockDim.x) in.cnt[j][i] = 0;
-  if (threadIdx.x == 0) *in.queue = 0;
+  if (threadIdx.x == 0) {
+    *in.queue = 0;
+    if (in.trace) vm_trace_rec(in.trace, 8, t0);
+  }
 }
 
 // VM_PDL=0 disables programmatic dependent launch (A/B).
@@ -1015,6 +1020,7 @@ extern "C" int vm_train_step(const VmStack* stacks, const VmBatch* batches, int 
         in.n_cnt[i] = pl.kp.s[i].K;
       }
     in.queue = reinterpret_cast<int*>(ws + pl.off_queue);
+    in.trace = trace_ptr();
     step_init_kernel<<<1, 256, 0, s>>>(in);
     VM_CUDA(cudaGetLastError());
     if (g_prof.on) g_prof.kernels += 1;

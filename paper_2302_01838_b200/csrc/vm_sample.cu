@@ -745,11 +745,41 @@ using namespace vm;
 extern "C" void vm_profile_count_kernels(int n);
 
 namespace vm {
-__global__ void step_advance_kernel(int64_t* c, int64_t inc) { *c += inc; }
+__global__ void step_advance_kernel(int64_t* c, int64_t inc, unsigned long long* tr) {
+  const unsigned long long t0 = tr ? vm_gtime() : 0;
+  *c += inc;
+  if (tr) vm_trace_rec(tr, 9, t0);
+}
 }  // namespace vm
 
+namespace vm {
+// End of a step graph: the step's result words (losses + status) stored
+// straight into mapped pinned host memory (no copy-engine transfer: a few
+// hundred bytes of posted writes) and the device step counter advanced.
+__global__ void step_finish_kernel(const int32_t* __restrict__ src, int32_t* host_dst, int n, int64_t* c,
+                                   int64_t inc, unsigned long long* tr) {
+  const unsigned long long t0 = tr ? vm_gtime() : 0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) host_dst[i] = __ldcg(src + i);
+  __threadfence_system();
+  if (threadIdx.x == 0) {
+    *c += inc;
+    if (tr) vm_trace_rec(tr, 9, t0);
+  }
+}
+}  // namespace vm
+
+extern "C" int vm_step_finish(const int32_t* words, int32_t* host_words, int32_t n_words, int64_t* counter,
+                              int64_t inc, void* stream) {
+  VM_REQUIRE(n_words >= 0 && (n_words == 0 || (words && host_words)) && counter, "vm_step_finish: bad arguments");
+  int32_t* dst = nullptr;
+  if (n_words > 0) VM_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&dst), host_words, 0));
+  step_finish_kernel<<<1, 256, 0, cudaStream_t(stream)>>>(words, dst, n_words, counter, inc, trace_ptr());
+  VM_CUDA(cudaGetLastError());
+  return VM_OK;
+}
+
 extern "C" int vm_step_advance(int64_t* counter, int64_t inc, void* stream) {
-  step_advance_kernel<<<1, 1, 0, cudaStream_t(stream)>>>(counter, inc);
+  step_advance_kernel<<<1, 1, 0, cudaStream_t(stream)>>>(counter, inc, trace_ptr());
   VM_CUDA(cudaGetLastError());
   return VM_OK;
 }

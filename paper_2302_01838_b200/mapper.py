@@ -402,11 +402,14 @@ class Mapper:
                             sample_obj(1 - p, 1)
                         with torch.cuda.stream(side_bg):
                             sample_bg(1 - p, 1)
-                    host_io.copy_(self._ws.results(n, n_st), non_blocking=True)  # losses + status, one copy
                     cur.wait_stream(side)
                     cur.wait_stream(side_bg)
-                    _lib.check(_lib.load().vm_step_advance(step_dev.data_ptr(), 1, _lib.stream_ptr()),
-                               "vm_step_advance")
+                    # losses + status straight into pinned host memory, and the
+                    # device step counter bump, in one kernel
+                    res = self._ws.results(n, n_st)
+                    _lib.check(_lib.load().vm_step_finish(res.data_ptr(), host_io.data_ptr(), res.numel(),
+                                                          step_dev.data_ptr(), 1, _lib.stream_ptr()),
+                               "vm_step_finish")
             graphs.append(g)
         self._g = dict(key=self._graph_key(), graphs=graphs, step_dev=step_dev, host_l=host_l, host_s=host_s,
                        stacks=[stacks(0), stacks(1)], sample=sample, next_ready=None,

@@ -450,6 +450,20 @@ def main():
     e2e_value = k_total * args.steps / float(e2e_s.item())
     d2h = mapper.last_io_bytes()[1]
     h2d = -(-(mapper.arena.uploaded_bytes - b0 + tables) // args.steps)  # crops + tables, per step
+    # the same public call without map growth: the reference arm's workload
+    # (its Mapper.train_step loop, no new keyframes), for the like-for-like ratio
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    t0 = time.perf_counter()
+    for i in range(args.steps):
+        rep = mapper.train_step()
+        shard.gather_losses(rep)
+    torch.cuda.synchronize()
+    e2e_t = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+    if world > 1:
+        torch.distributed.all_reduce(e2e_t, op=torch.distributed.ReduceOp.MAX)
+    e2e_train_only = k_total * args.steps / float(e2e_t.item())
 
     # rooflines: algorithmic FLOPs per launch / CUDA-event duration of that
     # launch (same step, eager replay with L2 flushed).  KF (objects, FP32
@@ -512,7 +526,10 @@ def main():
             "scaling": "weak" if args.workload == "2" else "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": _config(world, args.workload),
             "samples_per_s": (rays_obj / max(k_local, 1)) * value * cfg.points_per_ray,
-            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "includes": "Mapper.train_step per step + every steps_per_frame steps a frame's map growth "
+                                "(new keyframes for 10% of objects: crops H2D, tables rebuilt, batch redrawn)",
+                    "train_only": e2e_train_only},
             "gpu_launches": kernels_per_step * args.steps,
             "roofline": dominant,
             "roofline_kernels": kernels,

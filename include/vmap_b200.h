@@ -174,7 +174,10 @@ int vm_render_backward(int64_t n_rays, int32_t n_points, const float* occ, const
                        const float* t, const float* weights, const float* trans,
                        const float* grad_opacity, const float* grad_depth,
                        const float* grad_colour, float* d_occ, float* d_col, void* stream);
-/* ---- render.py:284-333 L1 losses (pairwise-summed over rays) and grads. --- */
+/* ---- render.py:284-333 L1 losses (pairwise-summed over rays) and grads. ---
+ * The per-ray terms live in a stream-ordered temporary (cudaMallocAsync /
+ * cudaFreeAsync on `stream`, 12 B per ray): the one entry point here that
+ * allocates; vm_train_step takes them from its caller's workspace. */
 int vm_losses(int32_t n_models, int32_t n_rays, const float* opacity, const float* depth,
               const float* colour, const float* target_depth, const float* target_colour,
               const uint8_t* target_mask, const uint8_t* valid_depth, const uint8_t* ray_ok,

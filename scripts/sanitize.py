@@ -19,3 +19,30 @@ for _ in range(2):
     rep = m.train_step()
 torch.cuda.synchronize()
 print("ok", rep.step, len(rep.losses))
+
+# graph-replayed steps (init kernel, persistent KF32 + prefetch, KT + PDL
+# reduce, loss sums branch, split Adam, vm_step_finish)
+mg = Mapper(scene["intrinsics"], cfg, use_graphs=True)
+populate(mg, scene)
+for _ in range(3):
+    rep = mg.train_step()
+torch.cuda.synchronize()
+print("graph ok", rep.step, len(rep.losses))
+
+# inference (vm_query_grid / vm_eval_rays / vm_view_*) on the trained map
+from paper_2302_01838_b200.meshing import query_grid, render_view  # noqa: E402
+inst = mg.instance_for_model(0)
+query_grid(mg.obj_params, 0, inst.aabb.padded(0.1), inst.pe_scale, 16)
+render_view(mg.obj_params, mg.bg_params, mg.map, scene["intrinsics"], scene["background"]["keyframes"][0]["pose"],
+            samples_object=8, samples_background=8, samples_refine=4)
+torch.cuda.synchronize()
+print("infer ok")
+
+# checkpoint pack/unpack (vm_pack_stack)
+import tempfile  # noqa: E402
+from paper_2302_01838_b200.checkpoint import load_checkpoint, save_checkpoint  # noqa: E402
+with tempfile.TemporaryDirectory() as d:
+    save_checkpoint(Path(d) / "m.vobj", mg.obj_params, mg.obj_state, mg.bg_params, mg.bg_state, mg.map)
+    load_checkpoint(Path(d) / "m.vobj", device=mg.obj_params.arena.device)
+torch.cuda.synchronize()
+print("ckpt ok")

@@ -211,8 +211,12 @@ class Mapper:
         sc = np.array([float(i.pe_scale) for i in objs] + ([float(bg.pe_scale)] if bg is not None else []),
                       np.float32)
         regraph = self._g is None
-        unchanged = (not regraph and all(not d.changed for pair in self._dev_tables for d in pair)
-                     and self._last_scales is not None and np.array_equal(sc, self._last_scales))
+        same_len = self._last_scales is not None and len(sc) == len(self._last_scales)
+        obj_changed = (not same_len or any(d.changed for d in self._dev_tables[0])
+                       or not np.array_equal(sc[:K], self._last_scales[:K]))
+        bg_changed = (not same_len or any(d.changed for d in self._dev_tables[1])
+                      or not np.array_equal(sc[K:], self._last_scales[K:]))
+        unchanged = not regraph and not obj_changed and not bg_changed
         self._last_scales = sc
         if unchanged:
             # a refresh without edits (e.g. invalidate() after a frame that
@@ -241,7 +245,11 @@ class Mapper:
             for a, b in zip(self._g["bufs"], (self._buf_obj, self._buf_bg)):
                 if a is not None and b is not None:
                     a.pe_scale.copy_(b.pe_scale)
-            self._g["next_ready"] = None  # tables changed: drop the prefetched batch
+            # tables changed: drop the prefetched batch of the stack(s) concerned
+            if obj_changed:
+                self._g["next_ready_obj"] = None
+            if bg_changed:
+                self._g["next_ready_bg"] = None
         self._tables = (t_obj, t_bg)
         self._tables_gen += 1
         self._sig = sig
@@ -412,7 +420,8 @@ class Mapper:
                                "vm_step_finish")
             graphs.append(g)
         self._g = dict(key=self._graph_key(), graphs=graphs, step_dev=step_dev, host_l=host_l, host_s=host_s,
-                       stacks=[stacks(0), stacks(1)], sample=sample, next_ready=None,
+                       stacks=[stacks(0), stacks(1)], sample_obj=sample_obj, sample_bg=sample_bg,
+                       next_ready_obj=None, next_ready_bg=None,
                        bufs=(bufs_o[1], bufs_b[1]))
 
     def enqueue_graph_step(self, step: int):
@@ -435,10 +444,14 @@ class Mapper:
         p = step & 1
         if g.get("dev_step") != step:  # the graph bumps the device counter itself
             g["step_dev"].fill_(step)
-        if g["next_ready"] != step:  # no prefetched batch for this step: sample it now
-            g["sample"](p, 0)
+        # no prefetched batch for this step (first step, or that stack's map
+        # changed): sample it now
+        if g["next_ready_obj"] != step:
+            g["sample_obj"](p, 0)
+        if g["next_ready_bg"] != step:
+            g["sample_bg"](p, 0)
         g["graphs"][p].replay()
-        g["next_ready"] = step + 1
+        g["next_ready_obj"] = g["next_ready_bg"] = step + 1
         g["dev_step"] = step + 1
         for params, _, _ in g["stacks"][p]:
             params.version += 1

@@ -65,6 +65,13 @@ inline int compute_layout(const VmArch& a, VmLayout& L) {
   return VM_OK;
 }
 
+// ---------------------------------------------------------------- forward-only evaluation (vm_mlp.cu)
+// bytes of the tensor-core forward's weight image for `a` (0: FFMA forward)
+size_t fwd_image_bytes(const VmArch& a);
+// vm_forward with the caller's scratch for that image (nullptr: stream-ordered temporary)
+int forward_ws(const VmStack* st, const float* encoded, int64_t n_samples, float* occ, float* col, float* img,
+               cudaStream_t s);
+
 // ---------------------------------------------------------------- schedule tracing (VM_TRACE=1)
 unsigned long long* trace_ptr();  // host: VM_TRACE buffer or null (vm_mlp.cu)
 

@@ -305,15 +305,16 @@ using namespace vm;
 extern "C" size_t vm_infer_workspace_bytes(const VmArch* arch, int64_t chunk) {
   if (!arch || chunk <= 0) return 0;
   // points f32 [chunk,3] + encoded f32 [chunk,D] + occ [chunk] + col [chunk,3] + t f64 [chunk]
-  return size_t(chunk) * (12 + 4 * size_t(arch->input_dim) + 4 + 12 + 8) + 1024;
+  // + the tensor-core forward's weight image (hidden-128 models)
+  return size_t(chunk) * (12 + 4 * size_t(arch->input_dim) + 4 + 12 + 8) + 1024 + fwd_image_bytes(*arch) + 256;
 }
 
 namespace {
 struct InferWs {
-  float *pts, *enc, *occ, *col;
+  float *pts, *enc, *occ, *col, *img;
   double* t;
 };
-InferWs carve(void* ws, int64_t chunk, int D) {
+InferWs carve(void* ws, int64_t chunk, int D, size_t img_bytes) {
   char* p = static_cast<char*>(ws);
   auto take = [&](size_t b) {
     char* r = p;
@@ -326,6 +327,7 @@ InferWs carve(void* ws, int64_t chunk, int D) {
   w.enc = reinterpret_cast<float*>(take(size_t(chunk) * 4 * D));
   w.occ = reinterpret_cast<float*>(take(size_t(chunk) * 4));
   w.col = reinterpret_cast<float*>(take(size_t(chunk) * 12));
+  w.img = img_bytes ? reinterpret_cast<float*>(take(img_bytes)) : nullptr;
   return w;
 }
 }  // namespace
@@ -355,7 +357,7 @@ extern "C" int vm_query_grid(const VmStack* stack, int32_t model_index, const do
   const PE32 pe = make_pe(c, h, pe_scale, nf, inc, stack->arch.input_dim);
   const VmStack view = model_view(*stack, model_index, L.block);
   cudaStream_t s = cudaStream_t(stream);
-  const InferWs w = carve(workspace, chunk, stack->arch.input_dim);
+  const InferWs w = carve(workspace, chunk, stack->arch.input_dim, fwd_image_bytes(stack->arch));
   const int64_t total = int64_t(resolution[0]) * resolution[1] * resolution[2];
   const double3 bmin = make_double3(box_min[0], box_min[1], box_min[2]);
   const double3 bmax = make_double3(box_max[0], box_max[1], box_max[2]);
@@ -365,7 +367,7 @@ extern "C" int vm_query_grid(const VmStack* stack, int32_t model_index, const do
                                                      n, w.pts);
     encode_f32_kernel<<<blocks_for(n), kIT, 0, s>>>(w.pts, n, pe, w.enc);
     VM_CUDA(cudaGetLastError());
-    const int rc = vm_forward(&view, w.enc, n, occ_out + start, w.col, stream);
+    const int rc = forward_ws(&view, w.enc, n, occ_out + start, w.col, w.img, s);
     if (rc) return rc;
   }
   return VM_OK;
@@ -394,7 +396,7 @@ extern "C" int vm_eval_rays(const VmStack* stack, int32_t model_index, const dou
   const PE32 pe = make_pe(c, h, pe_scale, nf, inc, stack->arch.input_dim);
   const VmStack view = model_view(*stack, model_index, L.block);
   cudaStream_t s = cudaStream_t(stream);
-  const InferWs w = carve(workspace, chunk, stack->arch.input_dim);
+  const InferWs w = carve(workspace, chunk, stack->arch.input_dim, fwd_image_bytes(stack->arch));
   const double3 o = make_double3(origin[0], origin[1], origin[2]);
   const int64_t rays_per = chunk / n_samples;
   for (int64_t r0 = 0; r0 < n_rays; r0 += rays_per) {
@@ -404,7 +406,7 @@ extern "C" int vm_eval_rays(const VmStack* stack, int32_t model_index, const dou
                                                      w.pts, w.t);
     encode_f32_kernel<<<blocks_for(ns), kIT, 0, s>>>(w.pts, ns, pe, w.enc);
     VM_CUDA(cudaGetLastError());
-    int rc = vm_forward(&view, w.enc, ns, w.occ, w.col, stream);
+    int rc = forward_ws(&view, w.enc, ns, w.occ, w.col, w.img, cudaStream_t(stream));
     if (rc) return rc;
     composite_kernel<<<blocks_for(n), kIT, 0, s>>>(w.occ, w.col, w.t, n, n_samples, opacity, depth, colour, r0);
     VM_CUDA(cudaGetLastError());

@@ -777,6 +777,16 @@ bool kh32_enabled() {
   return on;
 }
 
+// Hidden-128 forward-only evaluation (vm_forward: inference grids and view
+// rays) on the tensor cores; VM_TC_FWD=0 keeps it on the FFMA forward kernel.
+bool tc_fwd_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("VM_TC_FWD");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 // The tensor-core path is the default for hidden-128 stacks; VM_TC=0 selects
 // the FFMA kernel for them (A/B measurements and the parity cross-check).
 bool tc_enabled() {
@@ -1273,7 +1283,8 @@ extern "C" int vm_train_step(const VmStack* stacks, const VmBatch* batches, int 
 
 namespace {
 int run_fwd_bwd(const VmStack* st, const float* encoded, int64_t n_samples, const float* gocc,
-                const float* gcol, float* occ, float* col, float* grads, bool backward, cudaStream_t s) {
+                const float* gcol, float* occ, float* col, float* grads, bool backward, cudaStream_t s,
+                float* img_ws = nullptr) {
   VM_REQUIRE(st && encoded && n_samples >= 0, "vm_forward/backward: bad arguments");
   KParams kp;
   std::memset(&kp, 0, sizeof(kp));
@@ -1307,6 +1318,26 @@ int run_fwd_bwd(const VmStack* st, const float* encoded, int64_t n_samples, cons
     if (backward && ks.K > 0) VM_CUDA(cudaMemsetAsync(grads, 0, size_t(ks.K) * ks.block * 4, s));
     return VM_OK;
   }
+  if (!backward && tc_enabled() && tc_fwd_enabled() && ks.H == 128 && ks.L == 4 && ks.D <= tck::kK0) {
+    // hidden-128 forward (background grids / view rays) on the tensor cores:
+    // the weight image (3xTF32 pre-split chunks) in a stream-ordered
+    // temporary, then the persistent tile loop
+    using TI = tck::Img<128, 4>;
+    float* img = img_ws;
+    if (!img) VM_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&img), sizeof(float) * TI::total * size_t(ks.K), s));
+    tck::tc_prep_kernel<128, 4><<<dim3(TI::n_chunks * 4, ks.K), 256, 0, s>>>(ks, img);
+    VM_CUDA(cudaGetLastError());
+    static int sms = 0;
+    if (!sms) VM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+    const int64_t tiles = (n_samples + tck::kTM - 1) / tck::kTM;
+    const int gx = int(std::max<int64_t>(1, std::min<int64_t>(tiles, (sms + ks.K - 1) / ks.K)));
+    const int smem = tck::FwdSmem<128, 4>::total;
+    VM_CUDA(cudaFuncSetAttribute(tck::tc_forward_kernel<128, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    tck::tc_forward_kernel<128, 4><<<dim3(gx, ks.K), tck::kTCThreads, smem, s>>>(ks, img, n_samples, occ, col);
+    VM_CUDA(cudaGetLastError());
+    if (!img_ws) VM_CUDA(cudaFreeAsync(img, s));
+    return VM_OK;
+  }
   KernelFn fn = backward ? pick_kernel<kBackward>(ks.H, ks.L, 0, 0) : pick_kernel<kForward>(ks.H, ks.L, 0, 0);
   if (!fn) {
     set_error("vm_forward/backward: no kernel for this architecture");
@@ -1319,6 +1350,20 @@ int run_fwd_bwd(const VmStack* st, const float* encoded, int64_t n_samples, cons
 extern "C" int vm_forward(const VmStack* st, const float* encoded, int64_t n_samples, float* occ, float* col,
                           void* stream) {
   return run_fwd_bwd(st, encoded, n_samples, nullptr, nullptr, occ, col, nullptr, false, cudaStream_t(stream));
+}
+
+size_t vm::fwd_image_bytes(const VmArch& a) {
+  // one model's pre-split image (the inference entry points evaluate one model view)
+  return (tc_enabled() && tc_fwd_enabled() && a.hidden > 64 && a.hidden <= 128 && a.n_layers == 4 &&
+          a.input_dim <= tck::kK0)
+             ? sizeof(float) * tck::Img<128, 4>::total
+             : 0;
+}
+
+int vm::forward_ws(const VmStack* st, const float* encoded, int64_t n_samples, float* occ, float* col, float* img,
+                   cudaStream_t s) {
+  return run_fwd_bwd(st, encoded, n_samples, nullptr, nullptr, occ, col, nullptr, false, s,
+                     st && st->count == 1 ? img : nullptr);
 }
 
 extern "C" int vm_backward(const VmStack* st, const float* encoded, int64_t n_samples, const float* grad_occ,

@@ -860,5 +860,240 @@ __global__ void __launch_bounds__(kTCThreads, 1)
   finalize_model(st, k, all_finite, true, reinterpret_cast<float*>(smem), kNS * kSlot / 4);
 }
 
+// ---------------------------------------------------------------------------
+// KT forward only (inference: occupancy grids, view rays; meshing.py:64-97,
+// :453-579): the same 3xTF32 tcgen05 layer GEMMs as KT's forward, as a
+// persistent kernel looping over 128-sample tiles (blockIdx.y = model).  No
+// activation is kept for a backward pass, so one TMEM accumulator (128
+// columns) suffices; the pre-split weight chunks stream from the L2-resident
+// image through the same 3-slot ring; every role walks the same chunk
+// schedule, tile after tile, with the ring/accumulator phases running on.
+template <int H, int L>
+struct FwdSmem {
+  static constexpr int ring = kNS * kSlot;
+  static constexpr int bias = ring;                      // (L-1)*H floats
+  static constexpr int w3t = bias + (L - 1) * H * 4;     // [H][4]
+  static constexpr int b3 = w3t + 4 * H * 4;             // 4 (+pad)
+  static constexpr int zp = b3 + 16;                     // [2 halves][4][kTM]
+  static constexpr int bars = (zp + 2 * 4 * kTM * 4 + 7) / 8 * 8;
+  static constexpr int tmem = bars + (3 * kNS + 1) * 8;
+  static constexpr int total = tmem + 16;
+};
+
+template <int H, int L, class F>
+__device__ __forceinline__ void for_each_fwd_chunk(F&& f) {
+  using I = Img<H, L>;
+  int j = 0;
+  f(j++, Chunk{0, 32, 4, H, 0, 1, 0, I::fwd_off(0), I::kC32});
+  f(j++, Chunk{0, 8, 1, H, 0, 0, 1, I::fwd_off(0) + I::kC32, I::kC8});
+  for (int l = 1; l <= L - 2; ++l)
+    for (int c = 0; c < H / 32; ++c)
+      f(j++, Chunk{0, 32, 4, H, 0, c == 0, c == H / 32 - 1, I::fwd_off(l) + c * I::kC32, I::kC32});
+}
+
+template <int H, int L>
+__global__ void __launch_bounds__(kTCThreads, 1)
+    tc_forward_kernel(const __grid_constant__ KStack st, const float* __restrict__ img_all, int64_t n,
+                      float* __restrict__ occ, float* __restrict__ col) {
+  static_assert(H == 128, "two 64-column halves per TMEM lane quadrant");
+  constexpr int HC = H / 2;
+  using I = Img<H, L>;
+  using SM = FwdSmem<H, L>;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int k = blockIdx.y;
+  const int64_t n_tiles = (n + kTM - 1) / kTM;
+  const float* __restrict__ img = img_all + int64_t(k) * I::total;
+  const float* __restrict__ Pk = st.params + int64_t(k) * st.block;
+
+  float* sBias = reinterpret_cast<float*>(smem + SM::bias);
+  float* sW3t = reinterpret_cast<float*>(smem + SM::w3t);
+  float* sB3 = reinterpret_cast<float*>(smem + SM::b3);
+  float* sZ = reinterpret_cast<float*>(smem + SM::zp);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + SM::bars);
+  uint64_t* empty = full + kNS;
+  uint64_t* wfull = empty + kNS;
+  uint64_t* accf = wfull + kNS;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + SM::tmem);
+
+  if (warp == 0) tc::tmem_alloc(tmem_slot, 128);
+  if (tid == 0) {
+    for (int s = 0; s < kNS; ++s) {
+      tc::mbar_init(&full[s], kComputeThr);
+      tc::mbar_init(&empty[s], 1);
+      tc::mbar_init(&wfull[s], 1);
+    }
+    tc::mbar_init(accf, 1);
+    tc::mbar_fence_init();
+  }
+  for (int l = 0; l < L - 1; ++l)
+    for (int i = tid; i < H; i += kTCThreads) sBias[l * H + i] = Pk[st.b_off[l] + i];
+  for (int i = tid; i < 4 * H; i += kTCThreads) sW3t[(i % H) * 4 + i / H] = Pk[st.w_off[L - 1] + i];
+  if (tid < 4) sB3[tid] = Pk[st.b_off[L - 1] + tid];
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tm = *tmem_slot;
+
+  if (warp == kCW) {
+    // ------------------------------------------------ MMA issuer (one thread)
+    if (lane == 0) {
+      uint32_t wpar = 0, j = 0;
+      for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+        for_each_fwd_chunk<H, L>([&](int, const Chunk& ci) {
+          const uint32_t s = j % kNS;
+          tc::mbar_wait(&full[s], (j / kNS) & 1);
+          tc::mbar_wait(&wfull[s], (wpar >> s) & 1);
+          wpar ^= 1u << s;
+          tc::fence_after_sync();
+          const uint32_t sa = tc::smem_u32(smem + s * kSlot);
+          const uint32_t idesc = tc::idesc_tf32(128, ci.n, false, false);
+          const int kw = ci.kw;
+          const uint32_t a_lo = sa + kTM * kw * 4, b_hi = sa + kHalfSlot, b_lo = b_hi + ci.n * kw * 4;
+          for (int ks = 0; ks < ci.nks; ++ks) {
+            const uint32_t o = ks * 256;
+            const uint64_t ah = tc::sdesc(sa + o, 128, kw * 32), al = tc::sdesc(a_lo + o, 128, kw * 32);
+            const uint64_t bh = tc::sdesc(b_hi + o, 128, kw * 32), bl = tc::sdesc(b_lo + o, 128, kw * 32);
+            tc::mma_tf32(tm, al, bh, idesc, (ci.first && ks == 0) ? 0u : 1u);
+            tc::mma_tf32(tm, ah, bl, idesc, 1u);
+            tc::mma_tf32(tm, ah, bh, idesc, 1u);
+          }
+          tc::mma_commit(&empty[s]);
+          if (ci.last) tc::mma_commit(accf);
+          ++j;
+        });
+      }
+    }
+    __syncwarp();
+  } else {
+    // ------------------------------------- compute warps: (quadrant q, half h)
+    const int q = warp & 3, h = warp >> 2;
+    const int row = 32 * q + lane;
+    const int c0 = h * HC;
+    const uint32_t tq = tm + (uint32_t(32 * q) << 16);
+    uint32_t it = 0, accn = 0;
+    auto acquire_w = [&](int w_off, int floats, int issuer_half) -> uint8_t* {
+      const uint32_t s = it % kNS;
+      if (it >= uint32_t(kNS)) tc::mbar_wait(&empty[s], ((it / kNS) - 1) & 1);
+      uint8_t* slot = smem + s * kSlot;
+      if (tid == issuer_half * 128) {
+        tc::mbar_arrive_tx(&wfull[s], uint32_t(floats * 4));
+        tc::bulk_g2s(slot + kHalfSlot, img + w_off, uint32_t(floats * 4), &wfull[s]);
+      }
+      return slot;
+    };
+    auto release = [&]() {
+      tc::fence_async_smem();
+      tc::fence_before_sync();
+      tc::mbar_arrive(&full[it % kNS]);
+      ++it;
+    };
+    auto wait_acc = [&]() {
+      tc::mbar_wait(accf, accn & 1);
+      ++accn;
+      tc::fence_after_sync();
+    };
+    auto stage_row = [&](uint8_t* slot, int kw, const auto& v, int n4) {
+      float* hi = reinterpret_cast<float*>(slot);
+      float* lo = reinterpret_cast<float*>(slot + kTM * kw * 4);
+#pragma unroll
+      for (int g = 0; g < 8; ++g) {
+        if (g < n4) {
+          float4 a, b;
+          split_fast(v[4 * g + 0], a.x, b.x);
+          split_fast(v[4 * g + 1], a.y, b.y);
+          split_fast(v[4 * g + 2], a.z, b.z);
+          split_fast(v[4 * g + 3], a.w, b.w);
+          const uint32_t o = tc::ilv_off(row, 4 * g, kw) / 4;
+          st4(hi + o, a);
+          st4(lo + o, b);
+        }
+      }
+    };
+    auto ld64 = [&](uint32_t ta, uint32_t tb, float (&va)[32], float (&vb)[32]) {
+      uint32_t r0[16], r1[16], r2[16], r3[16];
+      VM_TMEM_LD16(ta, r0);
+      VM_TMEM_LD16(ta + 16, r1);
+      VM_TMEM_LD16(tb, r2);
+      VM_TMEM_LD16(tb + 16, r3);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        va[j] = __uint_as_float(r0[j]);
+        va[16 + j] = __uint_as_float(r1[j]);
+        vb[j] = __uint_as_float(r2[j]);
+        vb[16 + j] = __uint_as_float(r3[j]);
+      }
+    };
+    for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+      const int64_t g = tile * kTM + row;
+      const bool valid = g < n;
+      {
+        float x0[kK0];
+        input_row(st, nullptr, int64_t(k) * n + g, valid, x0);
+        float xa[32], xb[8];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) xa[i] = x0[i];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) xb[i] = x0[32 + i];
+        uint8_t* s0 = acquire_w(I::fwd_off(0), I::kC32, 0);
+        if (h == 0) stage_row(s0, 32, xa, 8);
+        release();
+        uint8_t* s1 = acquire_w(I::fwd_off(0) + I::kC32, I::kC8, 1);
+        if (h == 1) stage_row(s1, 8, xb, 2);
+        release();
+      }
+#pragma unroll 1
+      for (int l = 0; l < L - 1; ++l) {
+        wait_acc();
+        float x[2][32];
+        ld64(tq + c0, tq + c0 + 32, x[0], x[1]);
+#pragma unroll
+        for (int gg = 0; gg < 2; ++gg)
+#pragma unroll
+          for (int j = 0; j < 32; ++j) x[gg][j] = relu_np(x[gg][j] + sBias[l * H + c0 + 32 * gg + j]);
+        if (l == L - 2) {  // output layer (4 logits), partial over the owned columns
+          float z[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+          for (int gg = 0; gg < 2; ++gg)
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const float4 w = ld4(sW3t + 4 * (c0 + 32 * gg + j));
+              z[0] = fmaf(w.x, x[gg][j], z[0]);
+              z[1] = fmaf(w.y, x[gg][j], z[1]);
+              z[2] = fmaf(w.z, x[gg][j], z[2]);
+              z[3] = fmaf(w.w, x[gg][j], z[3]);
+            }
+#pragma unroll
+          for (int o = 0; o < 4; ++o) sZ[(h * 4 + o) * kTM + row] = z[o];
+          break;
+        }
+#pragma unroll 1
+        for (int c = 0; c < H / 32; ++c) {
+          uint8_t* sl = acquire_w(I::fwd_off(l + 1) + c * I::kC32, I::kC32, c >> 1);
+          if ((c >> 1) == h) {
+            float v[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = (c & 1) ? x[1][j] : x[0][j];
+            stage_row(sl, 32, v, 8);
+          }
+          release();
+        }
+      }
+      compute_sync();
+      if (h == 0 && valid) {
+        const int64_t gk = int64_t(k) * n + g;
+        occ[gk] = sigmoid_f((sZ[0 * kTM + row] + sZ[4 * kTM + row]) + sB3[0]);
+#pragma unroll
+        for (int o = 1; o < 4; ++o) col[gk * 3 + o - 1] = sigmoid_f((sZ[o * kTM + row] + sZ[(4 + o) * kTM + row]) + sB3[o]);
+      }
+      compute_sync();  // sZ is rewritten by the next tile
+    }
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  if (warp == 0) tc::tmem_free(tm, 128);
+}
+
 }  // namespace tck
 }  // namespace vm

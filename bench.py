@@ -535,6 +535,10 @@ def main():
             "roofline_kernels": kernels,
             "mlp_phase": {"ms": kernel_ms, "flop": flop_launch,
                           "achieved_tflops": flop_launch / (kernel_ms * 1e-3) / 1e12,
+                          "frac_of_fp32_peak": flop_launch / (kernel_ms * 1e-3) / 1e12 / ffma_peak,
+                          "note": "the whole fused MLP (KF32 objects || KT background, fork..join): algorithmic "
+                                  "FLOPs / phase time against the FP32 FFMA peak, the roofline of the "
+                                  "reference's f32 arithmetic (north star: fused-MLP roofline)",
                           "reduce_adam_ms": per_tag.get(3)},
             "clocks": clk.summary(),
             "cpu_baseline": cpu,

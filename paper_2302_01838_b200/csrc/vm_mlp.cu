@@ -779,13 +779,14 @@ bool kh32_enabled() {
 
 // Hidden-128 forward-only evaluation (vm_forward: inference grids and view
 // rays) on the tensor cores; VM_TC_FWD=0 keeps it on the FFMA forward kernel.
-bool tc_fwd_enabled() {
-  static const bool on = [] {
+int tc_fwd_mode() {  // 0: FFMA forward, 1: one tile in flight, 2 (default): two
+  static const int m = [] {
     const char* e = std::getenv("VM_TC_FWD");
-    return !(e && e[0] == '0');
+    return e ? std::atoi(e) : 2;
   }();
-  return on;
+  return m;
 }
+bool tc_fwd_enabled() { return tc_fwd_mode() != 0; }
 
 // The tensor-core path is the default for hidden-128 stacks; VM_TC=0 selects
 // the FFMA kernel for them (A/B measurements and the parity cross-check).
@@ -1330,10 +1331,21 @@ int run_fwd_bwd(const VmStack* st, const float* encoded, int64_t n_samples, cons
     static int sms = 0;
     if (!sms) VM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
     const int64_t tiles = (n_samples + tck::kTM - 1) / tck::kTM;
-    const int gx = int(std::max<int64_t>(1, std::min<int64_t>(tiles, (sms + ks.K - 1) / ks.K)));
-    const int smem = tck::FwdSmem<128, 4>::total;
-    VM_CUDA(cudaFuncSetAttribute(tck::tc_forward_kernel<128, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    tck::tc_forward_kernel<128, 4><<<dim3(gx, ks.K), tck::kTCThreads, smem, s>>>(ks, img, n_samples, occ, col);
+    // two tiles in flight per CTA when each CTA gets at least two (VM_TC_FWD=1: one)
+    const bool two = tc_fwd_mode() == 2 && tiles >= 2 * int64_t(sms);
+    const int64_t groups = two ? (tiles + 1) / 2 : tiles;
+    const int gx = int(std::max<int64_t>(1, std::min<int64_t>(groups, (sms + ks.K - 1) / ks.K)));
+    if (two) {
+      const int smem = tck::FwdSmem<128, 4, 2>::total;
+      VM_CUDA(cudaFuncSetAttribute(tck::tc_forward_kernel<128, 4, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   smem));
+      tck::tc_forward_kernel<128, 4, 2><<<dim3(gx, ks.K), tck::kTCThreads, smem, s>>>(ks, img, n_samples, occ, col);
+    } else {
+      const int smem = tck::FwdSmem<128, 4, 1>::total;
+      VM_CUDA(cudaFuncSetAttribute(tck::tc_forward_kernel<128, 4, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   smem));
+      tck::tc_forward_kernel<128, 4, 1><<<dim3(gx, ks.K), tck::kTCThreads, smem, s>>>(ks, img, n_samples, occ, col);
+    }
     VM_CUDA(cudaGetLastError());
     if (!img_ws) VM_CUDA(cudaFreeAsync(img, s));
     return VM_OK;

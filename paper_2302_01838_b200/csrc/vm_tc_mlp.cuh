@@ -863,46 +863,47 @@ __global__ void __launch_bounds__(kTCThreads, 1)
 // ---------------------------------------------------------------------------
 // KT forward only (inference: occupancy grids, view rays; meshing.py:64-97,
 // :453-579): the same 3xTF32 tcgen05 layer GEMMs as KT's forward, as a
-// persistent kernel looping over 128-sample tiles (blockIdx.y = model).  No
-// activation is kept for a backward pass, so one TMEM accumulator (128
-// columns) suffices; the pre-split weight chunks stream from the L2-resident
-// image through the same 3-slot ring; every role walks the same chunk
-// schedule, tile after tile, with the ring/accumulator phases running on.
-template <int H, int L>
+// persistent kernel looping over groups of NT 128-sample tiles (blockIdx.y =
+// model).  No activation is kept for a backward pass, so each tile in flight
+// needs one TMEM accumulator (128 columns).  With NT = 2 the chunk stream
+// interleaves the two tiles layer by layer (L0 t0, L0 t1, L1 t0, L1 t1, ...),
+// so the tensor core runs one tile's GEMM while the compute warps drain and
+// stage the other's; every role walks the same order, group after group, with
+// the ring and accumulator phases running on.
+template <int H, int L, int NT>
 struct FwdSmem {
   static constexpr int ring = kNS * kSlot;
   static constexpr int bias = ring;                      // (L-1)*H floats
   static constexpr int w3t = bias + (L - 1) * H * 4;     // [H][4]
   static constexpr int b3 = w3t + 4 * H * 4;             // 4 (+pad)
-  static constexpr int zp = b3 + 16;                     // [2 halves][4][kTM]
-  static constexpr int bars = (zp + 2 * 4 * kTM * 4 + 7) / 8 * 8;
-  static constexpr int tmem = bars + (3 * kNS + 1) * 8;
+  static constexpr int zp = b3 + 16;                     // [NT][2 halves][4][kTM]
+  static constexpr int bars = (zp + NT * 2 * 4 * kTM * 4 + 7) / 8 * 8;
+  static constexpr int tmem = bars + (3 * kNS + NT) * 8;
   static constexpr int total = tmem + 16;
 };
 
-template <int H, int L, class F>
-__device__ __forceinline__ void for_each_fwd_chunk(F&& f) {
+// chunk c of layer li of the forward schedule (layer 0: 2 chunks, K = 32 + 8)
+template <int H, int L>
+__device__ __forceinline__ Chunk fwd_chunk(int li, int c) {
   using I = Img<H, L>;
-  int j = 0;
-  f(j++, Chunk{0, 32, 4, H, 0, 1, 0, I::fwd_off(0), I::kC32});
-  f(j++, Chunk{0, 8, 1, H, 0, 0, 1, I::fwd_off(0) + I::kC32, I::kC8});
-  for (int l = 1; l <= L - 2; ++l)
-    for (int c = 0; c < H / 32; ++c)
-      f(j++, Chunk{0, 32, 4, H, 0, c == 0, c == H / 32 - 1, I::fwd_off(l) + c * I::kC32, I::kC32});
+  if (li == 0) return c == 0 ? Chunk{0, 32, 4, H, 0, 1, 0, I::fwd_off(0), I::kC32}
+                             : Chunk{0, 8, 1, H, 0, 0, 1, I::fwd_off(0) + I::kC32, I::kC8};
+  return Chunk{0, 32, 4, H, 0, c == 0, c == H / 32 - 1, I::fwd_off(li) + c * I::kC32, I::kC32};
 }
 
-template <int H, int L>
+template <int H, int L, int NT>
 __global__ void __launch_bounds__(kTCThreads, 1)
     tc_forward_kernel(const __grid_constant__ KStack st, const float* __restrict__ img_all, int64_t n,
                       float* __restrict__ occ, float* __restrict__ col) {
   static_assert(H == 128, "two 64-column halves per TMEM lane quadrant");
+  static_assert(NT == 1 || NT == 2, "tiles in flight");
   constexpr int HC = H / 2;
   using I = Img<H, L>;
-  using SM = FwdSmem<H, L>;
+  using SM = FwdSmem<H, L, NT>;
   extern __shared__ __align__(1024) uint8_t smem[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int k = blockIdx.y;
-  const int64_t n_tiles = (n + kTM - 1) / kTM;
+  const int64_t n_groups = (n + int64_t(kTM) * NT - 1) / (int64_t(kTM) * NT);
   const float* __restrict__ img = img_all + int64_t(k) * I::total;
   const float* __restrict__ Pk = st.params + int64_t(k) * st.block;
 
@@ -913,17 +914,17 @@ __global__ void __launch_bounds__(kTCThreads, 1)
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + SM::bars);
   uint64_t* empty = full + kNS;
   uint64_t* wfull = empty + kNS;
-  uint64_t* accf = wfull + kNS;
+  uint64_t* accf = wfull + kNS;  // [NT]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + SM::tmem);
 
-  if (warp == 0) tc::tmem_alloc(tmem_slot, 128);
+  if (warp == 0) tc::tmem_alloc(tmem_slot, 128 * NT);
   if (tid == 0) {
     for (int s = 0; s < kNS; ++s) {
       tc::mbar_init(&full[s], kComputeThr);
       tc::mbar_init(&empty[s], 1);
       tc::mbar_init(&wfull[s], 1);
     }
-    tc::mbar_init(accf, 1);
+    for (int t = 0; t < NT; ++t) tc::mbar_init(&accf[t], 1);
     tc::mbar_fence_init();
   }
   for (int l = 0; l < L - 1; ++l)
@@ -939,29 +940,38 @@ __global__ void __launch_bounds__(kTCThreads, 1)
     // ------------------------------------------------ MMA issuer (one thread)
     if (lane == 0) {
       uint32_t wpar = 0, j = 0;
-      for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-        for_each_fwd_chunk<H, L>([&](int, const Chunk& ci) {
-          const uint32_t s = j % kNS;
-          tc::mbar_wait(&full[s], (j / kNS) & 1);
-          tc::mbar_wait(&wfull[s], (wpar >> s) & 1);
-          wpar ^= 1u << s;
-          tc::fence_after_sync();
-          const uint32_t sa = tc::smem_u32(smem + s * kSlot);
-          const uint32_t idesc = tc::idesc_tf32(128, ci.n, false, false);
-          const int kw = ci.kw;
-          const uint32_t a_lo = sa + kTM * kw * 4, b_hi = sa + kHalfSlot, b_lo = b_hi + ci.n * kw * 4;
-          for (int ks = 0; ks < ci.nks; ++ks) {
-            const uint32_t o = ks * 256;
-            const uint64_t ah = tc::sdesc(sa + o, 128, kw * 32), al = tc::sdesc(a_lo + o, 128, kw * 32);
-            const uint64_t bh = tc::sdesc(b_hi + o, 128, kw * 32), bl = tc::sdesc(b_lo + o, 128, kw * 32);
-            tc::mma_tf32(tm, al, bh, idesc, (ci.first && ks == 0) ? 0u : 1u);
-            tc::mma_tf32(tm, ah, bl, idesc, 1u);
-            tc::mma_tf32(tm, ah, bh, idesc, 1u);
+      for (int64_t grp = blockIdx.x; grp < n_groups; grp += gridDim.x) {
+#pragma unroll 1
+        for (int li = 0; li < L - 1; ++li)
+#pragma unroll 1
+          for (int t = 0; t < NT; ++t) {
+            const uint32_t d = tm + uint32_t(t * 128);
+            const int nc = li == 0 ? 2 : H / 32;
+#pragma unroll 1
+            for (int c = 0; c < nc; ++c) {
+              const Chunk ci = fwd_chunk<H, L>(li, c);
+              const uint32_t s = j % kNS;
+              tc::mbar_wait(&full[s], (j / kNS) & 1);
+              tc::mbar_wait(&wfull[s], (wpar >> s) & 1);
+              wpar ^= 1u << s;
+              tc::fence_after_sync();
+              const uint32_t sa = tc::smem_u32(smem + s * kSlot);
+              const uint32_t idesc = tc::idesc_tf32(128, ci.n, false, false);
+              const int kw = ci.kw;
+              const uint32_t a_lo = sa + kTM * kw * 4, b_hi = sa + kHalfSlot, b_lo = b_hi + ci.n * kw * 4;
+              for (int ks = 0; ks < ci.nks; ++ks) {
+                const uint32_t o = ks * 256;
+                const uint64_t ah = tc::sdesc(sa + o, 128, kw * 32), al = tc::sdesc(a_lo + o, 128, kw * 32);
+                const uint64_t bh = tc::sdesc(b_hi + o, 128, kw * 32), bl = tc::sdesc(b_lo + o, 128, kw * 32);
+                tc::mma_tf32(d, al, bh, idesc, (ci.first && ks == 0) ? 0u : 1u);
+                tc::mma_tf32(d, ah, bl, idesc, 1u);
+                tc::mma_tf32(d, ah, bh, idesc, 1u);
+              }
+              tc::mma_commit(&empty[s]);
+              if (ci.last) tc::mma_commit(&accf[t]);
+              ++j;
+            }
           }
-          tc::mma_commit(&empty[s]);
-          if (ci.last) tc::mma_commit(accf);
-          ++j;
-        });
       }
     }
     __syncwarp();
@@ -971,7 +981,9 @@ __global__ void __launch_bounds__(kTCThreads, 1)
     const int row = 32 * q + lane;
     const int c0 = h * HC;
     const uint32_t tq = tm + (uint32_t(32 * q) << 16);
-    uint32_t it = 0, accn = 0;
+    uint32_t it = 0, accn[NT];
+#pragma unroll
+    for (int t = 0; t < NT; ++t) accn[t] = 0;
     auto acquire_w = [&](int w_off, int floats, int issuer_half) -> uint8_t* {
       const uint32_t s = it % kNS;
       if (it >= uint32_t(kNS)) tc::mbar_wait(&empty[s], ((it / kNS) - 1) & 1);
@@ -987,11 +999,6 @@ __global__ void __launch_bounds__(kTCThreads, 1)
       tc::fence_before_sync();
       tc::mbar_arrive(&full[it % kNS]);
       ++it;
-    };
-    auto wait_acc = [&]() {
-      tc::mbar_wait(accf, accn & 1);
-      ++accn;
-      tc::fence_after_sync();
     };
     auto stage_row = [&](uint8_t* slot, int kw, const auto& v, int n4) {
       float* hi = reinterpret_cast<float*>(slot);
@@ -1018,19 +1025,20 @@ __global__ void __launch_bounds__(kTCThreads, 1)
       VM_TMEM_LD16(tb + 16, r3);
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        va[j] = __uint_as_float(r0[j]);
-        va[16 + j] = __uint_as_float(r1[j]);
-        vb[j] = __uint_as_float(r2[j]);
-        vb[16 + j] = __uint_as_float(r3[j]);
+      for (int jj = 0; jj < 16; ++jj) {
+        va[jj] = __uint_as_float(r0[jj]);
+        va[16 + jj] = __uint_as_float(r1[jj]);
+        vb[jj] = __uint_as_float(r2[jj]);
+        vb[16 + jj] = __uint_as_float(r3[jj]);
       }
     };
-    for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-      const int64_t g = tile * kTM + row;
-      const bool valid = g < n;
-      {
+    for (int64_t grp = blockIdx.x; grp < n_groups; grp += gridDim.x) {
+      // layer-0 operands of every tile of the group
+#pragma unroll 1
+      for (int t = 0; t < NT; ++t) {
+        const int64_t g = (grp * NT + t) * kTM + row;
         float x0[kK0];
-        input_row(st, nullptr, int64_t(k) * n + g, valid, x0);
+        input_row(st, nullptr, int64_t(k) * n + g, g < n, x0);
         float xa[32], xb[8];
 #pragma unroll
         for (int i = 0; i < 32; ++i) xa[i] = x0[i];
@@ -1045,54 +1053,68 @@ __global__ void __launch_bounds__(kTCThreads, 1)
       }
 #pragma unroll 1
       for (int l = 0; l < L - 1; ++l) {
-        wait_acc();
-        float x[2][32];
-        ld64(tq + c0, tq + c0 + 32, x[0], x[1]);
-#pragma unroll
-        for (int gg = 0; gg < 2; ++gg)
-#pragma unroll
-          for (int j = 0; j < 32; ++j) x[gg][j] = relu_np(x[gg][j] + sBias[l * H + c0 + 32 * gg + j]);
-        if (l == L - 2) {  // output layer (4 logits), partial over the owned columns
-          float z[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll 1
+        for (int t = 0; t < NT; ++t) {
+          tc::mbar_wait(&accf[t], accn[t] & 1);
+          ++accn[t];
+          tc::fence_after_sync();
+          float x[2][32];
+          ld64(tq + uint32_t(t * 128) + c0, tq + uint32_t(t * 128) + c0 + 32, x[0], x[1]);
 #pragma unroll
           for (int gg = 0; gg < 2; ++gg)
 #pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              const float4 w = ld4(sW3t + 4 * (c0 + 32 * gg + j));
-              z[0] = fmaf(w.x, x[gg][j], z[0]);
-              z[1] = fmaf(w.y, x[gg][j], z[1]);
-              z[2] = fmaf(w.z, x[gg][j], z[2]);
-              z[3] = fmaf(w.w, x[gg][j], z[3]);
-            }
+            for (int jj = 0; jj < 32; ++jj) x[gg][jj] = relu_np(x[gg][jj] + sBias[l * H + c0 + 32 * gg + jj]);
+          if (l == L - 2) {  // output layer (4 logits), partial over the owned columns
+            float z[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-          for (int o = 0; o < 4; ++o) sZ[(h * 4 + o) * kTM + row] = z[o];
-          break;
-        }
-#pragma unroll 1
-        for (int c = 0; c < H / 32; ++c) {
-          uint8_t* sl = acquire_w(I::fwd_off(l + 1) + c * I::kC32, I::kC32, c >> 1);
-          if ((c >> 1) == h) {
-            float v[32];
+            for (int gg = 0; gg < 2; ++gg)
 #pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] = (c & 1) ? x[1][j] : x[0][j];
-            stage_row(sl, 32, v, 8);
+              for (int jj = 0; jj < 32; ++jj) {
+                const float4 w = ld4(sW3t + 4 * (c0 + 32 * gg + jj));
+                z[0] = fmaf(w.x, x[gg][jj], z[0]);
+                z[1] = fmaf(w.y, x[gg][jj], z[1]);
+                z[2] = fmaf(w.z, x[gg][jj], z[2]);
+                z[3] = fmaf(w.w, x[gg][jj], z[3]);
+              }
+#pragma unroll
+            for (int o = 0; o < 4; ++o) sZ[((t * 2 + h) * 4 + o) * kTM + row] = z[o];
+            continue;
           }
-          release();
+#pragma unroll 1
+          for (int c = 0; c < H / 32; ++c) {
+            uint8_t* sl = acquire_w(I::fwd_off(l + 1) + c * I::kC32, I::kC32, c >> 1);
+            if ((c >> 1) == h) {
+              float v[32];
+#pragma unroll
+              for (int jj = 0; jj < 32; ++jj) v[jj] = (c & 1) ? x[1][jj] : x[0][jj];
+              stage_row(sl, 32, v, 8);
+            }
+            release();
+          }
         }
       }
       compute_sync();
-      if (h == 0 && valid) {
-        const int64_t gk = int64_t(k) * n + g;
-        occ[gk] = sigmoid_f((sZ[0 * kTM + row] + sZ[4 * kTM + row]) + sB3[0]);
+      if (h == 0) {
+#pragma unroll 1
+        for (int t = 0; t < NT; ++t) {
+          const int64_t g = (grp * NT + t) * kTM + row;
+          if (g < n) {
+            const int64_t gk = int64_t(k) * n + g;
+            const float* z0 = sZ + (t * 2 + 0) * 4 * kTM;
+            const float* z1 = sZ + (t * 2 + 1) * 4 * kTM;
+            occ[gk] = sigmoid_f((z0[row] + z1[row]) + sB3[0]);
 #pragma unroll
-        for (int o = 1; o < 4; ++o) col[gk * 3 + o - 1] = sigmoid_f((sZ[o * kTM + row] + sZ[(4 + o) * kTM + row]) + sB3[o]);
+            for (int o = 1; o < 4; ++o)
+              col[gk * 3 + o - 1] = sigmoid_f((z0[o * kTM + row] + z1[o * kTM + row]) + sB3[o]);
+          }
+        }
       }
-      compute_sync();  // sZ is rewritten by the next tile
+      compute_sync();  // sZ is rewritten by the next group
     }
   }
   tc::fence_before_sync();
   __syncthreads();
-  if (warp == 0) tc::tmem_free(tm, 128);
+  if (warp == 0) tc::tmem_free(tm, 128 * NT);
 }
 
 }  // namespace tck

@@ -199,3 +199,22 @@ def test_kh32_tensor_path_opt_in(cuda):
     r = subprocess.run([sys.executable, "-c", KH32_SCRIPT, str(root)], env=env, capture_output=True, text=True,
                        timeout=600)
     assert r.returncode == 0 and "kh32 ok" in r.stdout, r.stdout + r.stderr
+
+
+def test_adam_corrections_past_the_table(cuda):
+    """Step counters past the host bias-correction table (beta2 so close to 1
+    that f32(1 - beta2**t) is not yet 1.0f at 2**18 steps): the kernels
+    evaluate models.py:434-436 with the device pow and still match the
+    reference update."""
+    arch = ModelArch(n_layers=3, hidden=16, n_freq=3)
+    params, state = init_stacked(arch, 2, seed=3, beta2=0.99999999)
+    ost = O.new_stack(oracle_arch(arch), 2, 3, beta2=0.99999999)
+    state.step[:2] = 300000
+    ost.step[:2] = 300000
+    batch = _synthetic_batch(arch, 2, 24, 6, seed=5)
+    hb = to_host_batch(batch)
+    for _ in range(2):
+        train_on_batch(params, state, batch, LossWeights())
+        O.train_on_batch(ost, hb)
+    assert_params_close(params, ost)
+    np.testing.assert_array_equal(state.step[:2].cpu().numpy(), ost.step[:2])

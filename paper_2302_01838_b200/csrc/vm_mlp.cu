@@ -108,6 +108,9 @@ __global__ void __launch_bounds__(kRedThreads, 6) reduce_partials_kernel(const _
   // launched with programmatic stream serialization behind KT: the CTAs may
   // be resident before KT finishes and wait here for its partials
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  // let the Adam grid queued behind this one be scheduled now (it waits on
+  // griddepcontrol.wait for this grid's completion before reading)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   extern __shared__ __align__(16) float red_smem[];
   __shared__ float4 gsum[kRedGroups][kRedChunk / 4];
   int b = blockIdx.x, si = 0;
@@ -191,7 +194,23 @@ __global__ void __launch_bounds__(kRedThreads, 6) reduce_partials_kernel(const _
 struct LeafTable {
   int n;
   int start[64], len[64];
+  int n_ops;
+  unsigned char ops[128];  // postfix of pairwise_combine: 0 = push the next leaf sum, 1 = add the top two
 };
+
+// postfix program of pairwise_combine(n) (vm_common.cuh): leaves (n <= 128)
+// push, inner nodes add their left and right results in that order
+void combine_program(int64_t n, LeafTable& lt) {
+  if (n <= 128) {
+    lt.ops[lt.n_ops++] = 0;
+    return;
+  }
+  int64_t n2 = n / 2;
+  n2 -= n2 % 8;
+  combine_program(n2, lt);
+  combine_program(n - n2, lt);
+  lt.ops[lt.n_ops++] = 1;
+}
 
 // Loss sums of a tensor-core stack's models: one CTA per (model, loss term):
 // the column is staged in smem, each leaf of numpy's pairwise recursion is
@@ -224,8 +243,19 @@ __global__ void __launch_bounds__(128) loss_sums_kernel(const __grid_constant__ 
   if (tid < lt.n) lf_sum[tid] = pairwise_sum_leaf([&](int64_t r) { return ls_col[r]; }, lt.start[tid], lt.len[tid]);
   __syncthreads();
   if (tid == 0) {
-    int next = 0;
-    const float sum = pairwise_combine(R, lf_sum, next);
+    // the combine as a flat postfix program (no recursion): same additions,
+    // same order as pairwise_combine
+    float stk[8];
+    int sp = 0, next = 0;
+    for (int o = 0; o < lt.n_ops; ++o) {
+      if (lt.ops[o] == 0) {
+        stk[sp++] = lf_sum[next++];
+      } else {
+        const float b = stk[--sp];
+        stk[sp - 1] = __fadd_rn(stk[sp - 1], b);
+      }
+    }
+    const float sum = stk[0];
     st.losses[int64_t(k) * 3 + j] = sum;
     if (!isfinite(sum)) atomicMin(&st.status[1], k);
     if (p.trace) vm_trace_rec(p.trace, 7, t0);
@@ -565,6 +595,9 @@ struct AdamParams {
 
 __global__ void __launch_bounds__(256) adam_train_kernel(const __grid_constant__ AdamParams p, int block_offset) {
   const unsigned long long t_start = p.trace ? vm_gtime() : 0;
+  // programmatic launch behind the partial reduce: wait for its gradients
+  // (a no-op for an ordinary launch)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   struct Rec {  // schedule record at every exit
     const AdamParams& p;
     unsigned long long t;
@@ -1116,7 +1149,7 @@ extern "C" int vm_train_step(const VmStack* stacks, const VmBatch* batches, int 
   // concurrent callers on different threads or devices never share them
   struct SideRes {
     cudaStream_t side = nullptr;
-    cudaEvent_t fork = nullptr, join = nullptr, kt_done = nullptr, ls_done = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr, kt_done = nullptr, ls_done = nullptr, kf_done = nullptr;
     cudaStream_t side2 = nullptr;  // loss sums of the tensor-core stacks
   };
   static thread_local SideRes side_res[64];
@@ -1128,6 +1161,7 @@ extern "C" int vm_train_step(const VmStack* stacks, const VmBatch* batches, int 
   cudaEvent_t& ev_join = side_res[dev].join;
   cudaEvent_t& ev_kt = side_res[dev].kt_done;
   cudaEvent_t& ev_ls = side_res[dev].ls_done;
+  cudaEvent_t& ev_kf = side_res[dev].kf_done;
   cudaStream_t& side2 = side_res[dev].side2;
   bool forked = false;
   cudaStream_t ts = s;
@@ -1162,7 +1196,10 @@ extern "C" int vm_train_step(const VmStack* stacks, const VmBatch* batches, int 
       g_prof.kernels += 1;
       VM_CUDA(cudaEventRecord(kf1, s));
     }
-    return launch_adam(pl, s, 0, adam_split);
+    rc = launch_adam(pl, s, 0, adam_split);
+    if (rc) return rc;
+    if (forked) VM_CUDA(cudaEventRecord(ev_kf, s));
+    return VM_OK;
   };
   // launch order: the FFMA kernel goes first (measured 0.195 vs 0.207 ms per
   // graph-replayed config-2 step); VM_KT_FIRST=1 launches KT first instead
@@ -1200,6 +1237,7 @@ extern "C" int vm_train_step(const VmStack* stacks, const VmBatch* batches, int 
         }
         if (!ev_kt) {
           VM_CUDA(cudaEventCreateWithFlags(&ev_kt, cudaEventDisableTiming));
+          VM_CUDA(cudaEventCreateWithFlags(&ev_kf, cudaEventDisableTiming));
           VM_CUDA(cudaEventCreateWithFlags(&ev_ls, cudaEventDisableTiming));
           VM_CUDA(cudaStreamCreateWithFlags(&side2, cudaStreamNonBlocking));
         }
@@ -1233,6 +1271,26 @@ extern "C" int vm_train_step(const VmStack* stacks, const VmBatch* batches, int 
     rc = launch_reduce(pl, i, ts);
     if (rc) return rc;
   }
+  // the tensor-core stacks' Adam right behind their reduce on the branch
+  // (programmatic launch; it waits for KF32 + the FFMA stacks' Adam through
+  // ev_kf, since it reads their status words), so the step's tail does not
+  // pay the join before it
+  bool adam_on_branch = false;
+  if (forked && kf_done && adam_split < pl.adam_grid && pdl_enabled()) {
+    VM_CUDA(cudaStreamWaitEvent(ts, ev_kf, 0));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(pl.adam_grid - adam_split);
+    cfg.blockDim = dim3(256);
+    cfg.stream = ts;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    VM_CUDA(cudaLaunchKernelEx(&cfg, adam_train_kernel, pl.ap, adam_split));
+    if (g_prof.on) g_prof.kernels += 1;
+    adam_on_branch = true;
+  }
   // loss sums of the split tensor-core models: on a second branch once KT is
   // done, concurrently with their partial reduce and Adam (only the host
   // report needs them; Adam needs the reduce); joined after Adam
@@ -1250,6 +1308,8 @@ extern "C" int vm_train_step(const VmStack* stacks, const VmBatch* batches, int 
     int64_t st64[64];
     lt.n = pairwise_leaves(ks.R, st64, lt.len, 64);  // <= 64: ls_sep
     for (int l = 0; l < lt.n; ++l) lt.start[l] = int(st64[l]);
+    lt.n_ops = 0;
+    combine_program(ks.R, lt);  // 2 * leaves - 1 <= 127 ops, stack depth <= 7 (64 leaves)
     const int ls_smem = ks.R * 4;
     if (ls_smem > 48 * 1024)
       VM_CUDA(cudaFuncSetAttribute(loss_sums_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, ls_smem));
@@ -1272,8 +1332,10 @@ extern "C" int vm_train_step(const VmStack* stacks, const VmBatch* batches, int 
     g_prof.pair(r0, r1, 3);
     VM_CUDA(cudaEventRecord(r0, s));
   }
-  rc = launch_adam(pl, s, adam_split);
-  if (rc) return rc;
+  if (!adam_on_branch) {
+    rc = launch_adam(pl, s, adam_split);
+    if (rc) return rc;
+  }
   if (ls_forked) {
     VM_CUDA(cudaEventRecord(ev_ls, side2));
     VM_CUDA(cudaStreamWaitEvent(s, ev_ls, 0));

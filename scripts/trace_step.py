@@ -19,7 +19,7 @@ for _ in range(5):
     m.train_step()
 lib = _lib.load()
 flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
-KIND = {1: "KF item", 2: "KT tile", 3: "reduce", 4: "Adam", 5: "sample prep", 6: "sample rays", 7: "loss sums", 8: "step init", 9: "step advance"}
+KIND = {1: "KF item", 2: "KT tile", 3: "reduce", 4: "Adam", 5: "sample prep", 6: "sample rays", 7: "loss sums", 8: "step init", 9: "step advance", 10: "ls staged", 11: "ls leaves"}
 buf = (C.c_ulonglong * (4 << 16))()
 n = C.c_int()
 for rep in range(3):

@@ -318,6 +318,8 @@ int vm_train_grid(const VmStack* stacks, const VmBatch* batches, int n_stacks, i
 
 /* Device step counter used by graph-replayed steps: *counter += inc. */
 int vm_step_advance(int64_t* counter, int64_t inc, void* stream);
+/* Launch an instantiated CUDA graph (cudaGraphExec_t) on a stream. */
+int vm_graph_launch(void* graph_exec, void* stream);
 /* End of a captured step: copy n_words result words (losses + status) into
  * pinned host memory by device stores (no copy-engine transfer) and advance
  * the device step counter by inc. */

@@ -139,6 +139,7 @@ _SIGNATURES = {
                                 C.POINTER(C.c_int)]),
     "vm_step_advance": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p]),
     "vm_step_finish": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_int64, C.c_void_p]),
+    "vm_graph_launch": (C.c_int, [C.c_void_p, C.c_void_p]),
     "vm_last_error": (C.c_char_p, []),
     "vm_version": (C.c_char_p, []),
     "vm_ffma_peak": (C.c_int, [C.c_int, C.POINTER(C.c_float), C.c_void_p]),

@@ -778,6 +778,14 @@ extern "C" int vm_step_finish(const int32_t* words, int32_t* host_words, int32_t
   return VM_OK;
 }
 
+// Launch an instantiated CUDA graph (the Mapper's captured step) on `stream`
+// without the Python-side replay wrapper.
+extern "C" int vm_graph_launch(void* graph_exec, void* stream) {
+  VM_REQUIRE(graph_exec, "vm_graph_launch: null graph");
+  VM_CUDA(cudaGraphLaunch(cudaGraphExec_t(graph_exec), cudaStream_t(stream)));
+  return VM_OK;
+}
+
 extern "C" int vm_step_advance(int64_t* counter, int64_t inc, void* stream) {
   step_advance_kernel<<<1, 1, 0, cudaStream_t(stream)>>>(counter, inc, trace_ptr());
   VM_CUDA(cudaGetLastError());

@@ -419,7 +419,13 @@ class Mapper:
                                                           step_dev.data_ptr(), 1, _lib.stream_ptr()),
                                "vm_step_finish")
             graphs.append(g)
-        self._g = dict(key=self._graph_key(), graphs=graphs, step_dev=step_dev, host_l=host_l, host_s=host_s,
+        execs = []
+        for g in graphs:
+            try:
+                execs.append(int(g.raw_cuda_graph_exec()))
+            except (AttributeError, RuntimeError):
+                execs.append(0)
+        self._g = dict(execs=execs, key=self._graph_key(), graphs=graphs, step_dev=step_dev, host_l=host_l, host_s=host_s,
                        stacks=[stacks(0), stacks(1)], sample_obj=sample_obj, sample_bg=sample_bg,
                        next_ready_obj=None, next_ready_bg=None,
                        bufs=(bufs_o[1], bufs_b[1]))
@@ -450,7 +456,11 @@ class Mapper:
             g["sample_obj"](p, 0)
         if g["next_ready_bg"] != step:
             g["sample_bg"](p, 0)
-        g["graphs"][p].replay()
+        ex = g["execs"][p]
+        if ex:  # the instantiated graph straight through cudaGraphLaunch (no Python replay wrapper)
+            _lib.check(_lib.load().vm_graph_launch(ex, _lib.stream_ptr()), "vm_graph_launch")
+        else:
+            g["graphs"][p].replay()
         g["next_ready_obj"] = g["next_ready_bg"] = step + 1
         g["dev_step"] = step + 1
         for params, _, _ in g["stacks"][p]:

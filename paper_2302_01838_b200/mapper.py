@@ -456,7 +456,7 @@ class Mapper:
             g["sample_obj"](p, 0)
         if g["next_ready_bg"] != step:
             g["sample_bg"](p, 0)
-        ex = g["execs"][p]
+        ex = g["execs"][p] if _DIRECT_LAUNCH else 0
         if ex:  # the instantiated graph straight through cudaGraphLaunch (no Python replay wrapper)
             _lib.check(_lib.load().vm_graph_launch(ex, _lib.stream_ptr()), "vm_graph_launch")
         else:
@@ -555,6 +555,9 @@ class Mapper:
         self.global_step += 1
         return StepReport(step=step, frame_id=self.last_frame_id, k_models=k_models, losses=report_losses,
                           total=float(total), ms=(time.perf_counter() - t0) * 1e3)
+
+
+X
 
 
 def run_mapping(dataset, cfg: TrainConfig | None = None, mode: str = "vectorised", progress: bool = False,

@@ -1278,6 +1278,8 @@ extern "C" int vm_train_step(const VmStack* stacks, const VmBatch* batches, int 
   bool adam_on_branch = false;
   if (forked && kf_done && adam_split < pl.adam_grid && pdl_enabled()) {
     VM_CUDA(cudaStreamWaitEvent(ts, ev_kf, 0));
+    // the MLP phase (profile tag 0) ends here: KF32 + its Adam and KT + reduce done
+    if (g_prof.on) VM_CUDA(cudaEventRecord(e1, ts));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(pl.adam_grid - adam_split);
     cfg.blockDim = dim3(256);
@@ -1326,7 +1328,7 @@ extern "C" int vm_train_step(const VmStack* stacks, const VmBatch* batches, int 
     VM_CUDA(cudaEventRecord(ev_join, side));
     VM_CUDA(cudaStreamWaitEvent(s, ev_join, 0));
   }
-  if (g_prof.on) VM_CUDA(cudaEventRecord(e1, s));
+  if (g_prof.on && !adam_on_branch) VM_CUDA(cudaEventRecord(e1, s));
   cudaEvent_t r0 = nullptr, r1 = nullptr;
   if (g_prof.on) {
     g_prof.pair(r0, r1, 3);

@@ -35,11 +35,13 @@ inline int hidden_pad_of(int hidden) {
   if (hidden <= 32) return 32;
   if (hidden <= 64) return 64;
   if (hidden <= 128) return 128;
+  if (hidden <= (1 << 16)) return round_up(hidden, 32);  // layered path only (vm_layered.cu)
   return -1;
 }
 
 // models.py:50-55 layer_dims, padded for the kernels: layer 0 fan-in to a
-// multiple of 4 floats (16 B rows), hidden widths to 32/64/128.
+// multiple of 4 floats (16 B rows), hidden widths to 32/64/128 (wider: a
+// multiple of 32, trained by the layered path).
 inline int compute_layout(const VmArch& a, VmLayout& L) {
   if (a.n_layers < 2 || a.n_layers > VM_MAX_LAYERS || a.hidden < 1 || a.input_dim < 1) return VM_ERR_SHAPE;
   const int hp = hidden_pad_of(a.hidden);
@@ -71,6 +73,15 @@ size_t fwd_image_bytes(const VmArch& a);
 // vm_forward with the caller's scratch for that image (nullptr: stream-ordered temporary)
 int forward_ws(const VmStack* st, const float* encoded, int64_t n_samples, float* occ, float* col, float* img,
                cudaStream_t s);
+
+// ---------------------------------------------------------------- layered path (vm_layered.cu)
+// Architectures / batches without a fused kernel: one kernel sequence per layer.
+bool layered_forced();
+size_t layered_train_bytes(const VmStack* stacks, const VmBatch* batches, int n, int first);
+int train_layered(const VmStack* stacks, const VmBatch* batches, int n, int first, VmLossWeights w, float* losses,
+                  int32_t* status, void* workspace, size_t workspace_bytes, cudaStream_t s);
+int layered_fwd_bwd(const VmStack& st, const float* enc, int64_t n_samples, const float* gocc, const float* gcol,
+                    float* occ, float* col, float* grads, bool backward, cudaStream_t s);
 
 // ---------------------------------------------------------------- schedule tracing (VM_TRACE=1)
 unsigned long long* trace_ptr();  // host: VM_TRACE buffer or null (vm_mlp.cu)

@@ -1010,10 +1010,45 @@ extern "C" int vm_work_items(const int32_t* model_rays, int32_t n_models, int32_
   return VM_OK;
 }
 
-extern "C" size_t vm_train_workspace_bytes(const VmStack* stacks, const VmBatch* batches, int n_stacks) {
+// Whether the fused kernels (KF32 / generic FFMA, KT) take every stack of
+// this call; otherwise the layered path (vm_layered.cu) trains the stacks the
+// fused kernels lack.
+static bool fused_supported(const VmStack* stacks, const VmBatch* batches, int n) {
+  if (layered_forced()) return false;
   TrainPlan pl;
-  if (plan_train(stacks, batches, n_stacks, pl)) return 0;
+  if (plan_train(stacks, batches, n, pl)) return false;
+  KParams kf;
+  std::memset(&kf, 0, sizeof(kf));
+  for (int i = 0; i < n; ++i)
+    if (!pl.kp.s[i].tc) kf.s[kf.n_stacks++] = pl.kp.s[i];
+  if (kf.n_stacks == 0) return true;
+  if (kf32_enabled() && kf32_supported(kf)) return true;
+  return pick_kernel<kTrain>(kf.s[0].H, kf.s[0].L, kf.n_stacks > 1 ? kf.s[1].H : 0,
+                             kf.n_stacks > 1 ? kf.s[1].L : 0) != nullptr &&
+         pl.smem <= 227 * 1024;
+}
+
+// 0: every stack fused; 1: stack 0 fused, stack 1 layered; 2: all layered
+// (a layered stack 0 would have to precede a fused stack 1, whose kernels
+// read stack 0's status words inside the same fused launch sequence).
+static int train_route(const VmStack* stacks, const VmBatch* batches, int n) {
+  if (fused_supported(stacks, batches, n)) return 0;
+  if (n == 2 && fused_supported(stacks, batches, 1)) return 1;
+  return 2;
+}
+
+static size_t fused_bytes(const VmStack* stacks, const VmBatch* batches, int n) {
+  TrainPlan pl;
+  if (plan_train(stacks, batches, n, pl)) return 0;
   return pl.ws_bytes;
+}
+
+extern "C" size_t vm_train_workspace_bytes(const VmStack* stacks, const VmBatch* batches, int n_stacks) {
+  switch (train_route(stacks, batches, n_stacks)) {
+    case 0: return fused_bytes(stacks, batches, n_stacks);
+    case 1: return align_up(fused_bytes(stacks, batches, 1), 256) + layered_train_bytes(stacks, batches, 2, 1);
+    default: return layered_train_bytes(stacks, batches, n_stacks, 0);
+  }
 }
 
 // VM_TRACE=1: every vm_train_step records (kind 1 = FFMA item, 2 = KT tile,
@@ -1041,9 +1076,9 @@ namespace {
 unsigned long long* trace_buffer(cudaStream_t) { return vm::trace_ptr(); }
 }  // namespace
 
-extern "C" int vm_train_step(const VmStack* stacks, const VmBatch* batches, int n_stacks, VmLossWeights w,
-                             float* losses, int32_t* status, void* workspace, size_t workspace_bytes,
-                             void* stream) {
+static int train_fused(const VmStack* stacks, const VmBatch* batches, int n_stacks, VmLossWeights w,
+                       float* losses, int32_t* status, void* workspace, size_t workspace_bytes,
+                       void* stream) {
   TrainPlan pl;
   int rc = plan_train(stacks, batches, n_stacks, pl);
   if (rc) return rc;
@@ -1346,6 +1381,28 @@ extern "C" int vm_train_step(const VmStack* stacks, const VmBatch* batches, int 
   return VM_OK;
 }
 
+extern "C" int vm_train_step(const VmStack* stacks, const VmBatch* batches, int n_stacks, VmLossWeights w,
+                             float* losses, int32_t* status, void* workspace, size_t workspace_bytes,
+                             void* stream) {
+  VM_REQUIRE(stacks && batches && n_stacks >= 1 && n_stacks <= VM_MAX_STACKS,
+             "vm_train_step: 1 or 2 stacks supported");
+  const cudaStream_t s = cudaStream_t(stream);
+  switch (train_route(stacks, batches, n_stacks)) {
+    case 0:
+      return train_fused(stacks, batches, n_stacks, w, losses, status, workspace, workspace_bytes, stream);
+    case 1: {
+      const size_t b0 = align_up(fused_bytes(stacks, batches, 1), 256);
+      VM_REQUIRE(workspace_bytes >= b0, "vm_train_step: workspace too small");
+      int rc = train_fused(stacks, batches, 1, w, losses, status, workspace, b0, stream);
+      if (rc) return rc;
+      return train_layered(stacks, batches, 2, 1, w, losses, status, static_cast<char*>(workspace) + b0,
+                           workspace_bytes - b0, s);
+    }
+    default:
+      return train_layered(stacks, batches, n_stacks, 0, w, losses, status, workspace, workspace_bytes, s);
+  }
+}
+
 namespace {
 int run_fwd_bwd(const VmStack* st, const float* encoded, int64_t n_samples, const float* gocc,
                 const float* gcol, float* occ, float* col, float* grads, bool backward, cudaStream_t s,
@@ -1355,6 +1412,13 @@ int run_fwd_bwd(const VmStack* st, const float* encoded, int64_t n_samples, cons
   std::memset(&kp, 0, sizeof(kp));
   VmLayout L;
   int rc = fill_stack(*st, kp.s[0], L);
+  if (rc == VM_ERR_UNSUPPORTED || (!rc && !(kp.s[0].H == 128 && kp.s[0].L == 4 && !backward && tc_enabled() &&
+                                            tc_fwd_enabled() && kp.s[0].D <= tck::kK0) &&
+                                   !(backward ? pick_kernel<kBackward>(kp.s[0].H, kp.s[0].L, 0, 0)
+                                              : pick_kernel<kForward>(kp.s[0].H, kp.s[0].L, 0, 0)))) {
+    // no fused kernel for this architecture: one kernel sequence per layer
+    return layered_fwd_bwd(*st, encoded, n_samples, gocc, gcol, occ, col, grads, backward, s);
+  }
   if (rc) {
     set_error("vm_forward/backward: unsupported architecture");
     return rc;

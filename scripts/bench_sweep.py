@@ -42,6 +42,30 @@ if vobj is not None:
 out["fig6_train_only"] = fig6
 out["fig6_paper_rtx3090_ms"] = {"k50": 5.11, "k200": 14.70, "note": "PAPER.md:489/504, vMAP vectorised, hidden 32"}
 
+# ---------------- Fig. 6 (right): hidden widths beyond the fused kernels (layered path) ----------------
+paper_h = {16: 5.34, 32: 5.31, 64: 6.63, 128: 9.37, 256: 18.53, 512: 44.73, 1024: 155.88}
+cfg6 = TrainConfig()
+wide = benchmark([50], [256, 512, 1024], timed_steps=5 if quick else 20, warmup_steps=3, modes=("vectorised",))
+fig6h = []
+for r in [x for x in rows if x.k == 50] + wide:
+    arch = cfg6.arch_object
+    d = 3 * arch.include_input + 6 * arch.n_freq
+    h = r.hidden
+    macs = d * h + (arch.n_layers - 2) * h * h + 4 * h  # per sample
+    flop = 6.0 * cfg6.rays_per_object * cfg6.points_per_ray * macs * r.k  # forward + dW + dx
+    fig6h.append({"k": r.k, "hidden": h, "ms": r.ms, "tflops": flop / (r.ms * 1e-3) / 1e12,
+                  "paper_rtx3090_ms": paper_h.get(h), "path": "layered" if h > 128 else "fused"})
+if vobj is not None:
+    from vobj.trainer import benchmark as ref_benchmark
+    for r in ref_benchmark([50], [256], timed_steps=1, warmup_steps=1, modes=("vectorised",)):
+        for f in fig6h:
+            if f["hidden"] == r.hidden:
+                f["reference_cpu_ms"] = r.ms
+                f["speedup"] = r.ms / f["ms"]
+out["fig6_hidden_k50"] = fig6h
+out["fig6_hidden_note"] = ("PAPER.md:550-556 (K unstated; K=50 here), R=120, S=10, 4 layers; tflops = "
+                           "6 x samples x MACs per sample / step time (FP32 FFMA peak ~74)")
+
 # ---------------- inference ----------------
 from paper_2302_01838_b200.mapper import Mapper  # noqa: E402
 from paper_2302_01838_b200.meshing import query_grid, render_view  # noqa: E402

@@ -40,4 +40,14 @@ def test_layout_rejects_bad_arch():
     with pytest.raises(ValueError):
         _lib.layout(1, 32, 33)
     with pytest.raises(NotImplementedError):
-        _lib.layout(4, 256, 33)
+        _lib.layout(4, 1 << 17, 33)
+    with pytest.raises(ValueError):
+        _lib.layout(9, 32, 33)  # > VM_MAX_LAYERS
+
+
+def test_layout_wide_models():
+    """Widths above 128 (layered path): hidden rows padded to a multiple of 32."""
+    L = _lib.layout(4, 200, 63)
+    assert L.hidden_pad == 224
+    assert list(L.fi_pad[:4]) == [64, 224, 224, 224] and list(L.fo_pad[:4]) == [224, 224, 224, 4]
+    assert L.n_params == 200 * 63 + 200 + 2 * (200 * 200 + 200) + 4 * 200 + 4

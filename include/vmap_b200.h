@@ -49,15 +49,15 @@ extern "C" {
 /* models.py:19-55 ModelArch (output_dim is always 4: occupancy + RGB). */
 typedef struct VmArch {
   int32_t n_layers;   /* >= 2 */
-  int32_t hidden;     /* 1..128 */
-  int32_t input_dim;  /* 3*include_input + 6*n_freq, 1..60 */
+  int32_t hidden;     /* >= 1 (fused kernels: <= 128; wider: the layered path) */
+  int32_t input_dim;  /* 3*include_input + 6*n_freq (fused kernels: <= 40) */
   int32_t reserved;
 } VmArch;
 
 /* Arena layout of one model block, filled by vm_model_layout(). */
 typedef struct VmLayout {
   int32_t n_layers;
-  int32_t hidden_pad;                 /* 32, 64 or 128 */
+  int32_t hidden_pad;                 /* 32, 64, 128, else hidden rounded up to 32 */
   int32_t fo[VM_MAX_LAYERS], fi[VM_MAX_LAYERS];         /* true dims */
   int32_t fo_pad[VM_MAX_LAYERS], fi_pad[VM_MAX_LAYERS]; /* arena dims */
   int64_t w_off[VM_MAX_LAYERS], b_off[VM_MAX_LAYERS];   /* float offsets */
@@ -144,6 +144,13 @@ size_t vm_train_workspace_bytes(const VmStack* stacks, const VmBatch* batches, i
    sequential bits). */
 int vm_work_items(const int32_t* model_rays, int32_t n_models, int32_t n_points, int32_t* items,
                   int32_t capacity, int32_t* n_items);
+/* Stacks without a fused kernel (hidden > 128, input_dim > 40, n_points > 32
+   (up to 64), layer counts other than the fused instantiations) are trained by
+   the layered path: the same math one layer at a time (per-layer batched FP32
+   GEMMs, the per-ray render chain, Adam), with the same status words, skip
+   rules and vectorised == sequential bits; it requires `encoded`.  In a
+   two-stack call with a fused stack 0 only stack 1 takes it.  VM_LAYERED=1
+   forces it for every stack (cross-check). */
 int vm_train_step(const VmStack* stacks, const VmBatch* batches, int n_stacks,
                   VmLossWeights weights, float* losses /* [sum K][3] */,
                   int32_t* status /* device [4*n_stacks] */,

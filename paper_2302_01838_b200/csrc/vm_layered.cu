@@ -116,23 +116,28 @@ __global__ void __launch_bounds__(kGT) gemm_kernel(const __grid_constant__ Gemm 
   for (int k0 = k_begin; k0 < k_end; k0 += kBK) {
     const bool more = k0 + kBK < k_end;
     if (more) load(k0 + kBK);
-#pragma unroll
-    for (int kk = 0; kk < kBK; ++kk) {
-      float a[TM], b[TN];
+    // fragments of step kk+1 are read from smem while step kk's FFMAs issue
+    float a[2][TM], b[2][TN];
+    auto frag = [&](int kk, int f) {
 #pragma unroll
       for (int i = 0; i < TM; i += 4) {
         const float4 v = *reinterpret_cast<const float4*>(&As[buf][kk][ty * TM + i]);
-        a[i] = v.x, a[i + 1] = v.y, a[i + 2] = v.z, a[i + 3] = v.w;
+        a[f][i] = v.x, a[f][i + 1] = v.y, a[f][i + 2] = v.z, a[f][i + 3] = v.w;
       }
 #pragma unroll
       for (int j = 0; j < TN; j += 4) {
         const float4 v = *reinterpret_cast<const float4*>(&Bs[buf][kk][tx * TN + j]);
-        b[j] = v.x, b[j + 1] = v.y, b[j + 2] = v.z, b[j + 3] = v.w;
+        b[f][j] = v.x, b[f][j + 1] = v.y, b[f][j + 2] = v.z, b[f][j + 3] = v.w;
       }
+    };
+    frag(0, 0);
+#pragma unroll
+    for (int kk = 0; kk < kBK; ++kk) {
+      if (kk + 1 < kBK) frag(kk + 1, (kk + 1) & 1);
 #pragma unroll
       for (int i = 0; i < TM; ++i)
 #pragma unroll
-        for (int j = 0; j < TN; ++j) acc[i][j] = __fmaf_rn(a[i], b[j], acc[i][j]);
+        for (int j = 0; j < TN; ++j) acc[i][j] = __fmaf_rn(a[kk & 1][i], b[kk & 1][j], acc[i][j]);
     }
     if (more) store(buf ^ 1);
     __syncthreads();

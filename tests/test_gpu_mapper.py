@@ -57,6 +57,20 @@ def test_config1_with_background_losses(cuda):
     print("worst per-step loss rel diff", worst)
 
 
+def test_config1_wide_background(cuda):
+    """Mapper.train_step (graph-replayed) with a hidden-256 background: the
+    objects on KF32 and the background on the layered path inside the same
+    captured step; per-step losses over 5 steps and the background's
+    parameters against the oracle's map_update_step."""
+    from paper_2302_01838_b200 import ModelArch
+    from .helpers import assert_params_rel_l2
+    scene = config("1")
+    cfg = TrainConfig(arch_background=ModelArch(n_layers=4, hidden=256, n_freq=5))
+    m, ms, worst = _run(scene, cfg, 5)
+    print("worst per-step loss rel diff", worst)
+    assert_params_rel_l2(m.bg_params, ms.bg)
+
+
 def test_frozen_background_reports_zero_loss(cuda):
     scene = make_scene(2, n_kf=1, width=160, height=120, focal=80, crop=(20, 50), n_kf_bg=1, seed=2)
     m = Mapper(scene["intrinsics"], TrainConfig())

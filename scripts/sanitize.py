@@ -1,6 +1,7 @@
 """Small eager map-update run for compute-sanitizer (memcheck / racecheck /
 synccheck): config-1 scene, objects (KF32) + background (KT + partial reduce),
-sampler (KS) and Adam, plus the generic FFMA kernel (VM_KF32=0 runs)."""
+sampler (KS) and Adam, plus the generic FFMA kernel (VM_KF32=0 runs), inference,
+checkpoints and the layered path."""
 import sys
 from pathlib import Path
 
@@ -46,3 +47,19 @@ with tempfile.TemporaryDirectory() as d:
     load_checkpoint(Path(d) / "m.vobj", device=mg.obj_params.arena.device)
 torch.cuda.synchronize()
 print("ckpt ok")
+
+# layered path (vm_layered.cu): a hidden-256 background behind the fused
+# objects in one call, and the layered forward / backward entry points
+from paper_2302_01838_b200 import LossWeights, ModelArch, init_stacked  # noqa: E402
+from paper_2302_01838_b200.models import backward, forward  # noqa: E402
+from paper_2302_01838_b200.trainer import _synthetic_batch, launch_train  # noqa: E402
+ao, ab = ModelArch(hidden=32), ModelArch(hidden=200, n_layers=3)
+po, so = init_stacked(ao, 2, seed=0)
+pb, sb = init_stacked(ab, 1, seed=0, stream=2)
+bo, bb = _synthetic_batch(ao, 2, 40, 10, seed=3), _synthetic_batch(ab, 1, 70, 12, seed=4)
+for _ in range(2):
+    launch_train([(po, so, bo), (pb, sb, bb)], LossWeights())
+out, cache = forward(pb, torch.randn(1, 77, ab.input_dim))
+backward(pb, cache, torch.ones(1, 77), torch.ones(1, 77, 3))
+torch.cuda.synchronize()
+print("layered ok")

@@ -102,6 +102,11 @@ __global__ void __launch_bounds__(kGT) gemm_kernel(const __grid_constant__ Gemm 
     }
   };
   const int tx = tid % (BN / TN), ty = tid / (BN / TN);
+  // an 8-wide register block is two 4-wide halves BM/2 (BN/2) apart, so a
+  // warp's LDS.128 fragment reads cover contiguous 16-B chunks (a contiguous
+  // 8-float block per thread would put every fourth thread on the same banks)
+  auto row = [&](int i) { return TM == 8 ? (i & 4 ? BM / 2 : 0) + ty * 4 + (i & 3) : ty * TM + i; };
+  auto colx = [&](int j) { return TN == 8 ? (j & 4 ? BN / 2 : 0) + tx * 4 + (j & 3) : tx * TN + j; };
   float acc[TM][TN];
 #pragma unroll
   for (int i = 0; i < TM; ++i)
@@ -121,12 +126,12 @@ __global__ void __launch_bounds__(kGT) gemm_kernel(const __grid_constant__ Gemm 
     auto frag = [&](int kk, int f) {
 #pragma unroll
       for (int i = 0; i < TM; i += 4) {
-        const float4 v = *reinterpret_cast<const float4*>(&As[buf][kk][ty * TM + i]);
+        const float4 v = *reinterpret_cast<const float4*>(&As[buf][kk][row(i)]);
         a[f][i] = v.x, a[f][i + 1] = v.y, a[f][i + 2] = v.z, a[f][i + 3] = v.w;
       }
 #pragma unroll
       for (int j = 0; j < TN; j += 4) {
-        const float4 v = *reinterpret_cast<const float4*>(&Bs[buf][kk][tx * TN + j]);
+        const float4 v = *reinterpret_cast<const float4*>(&Bs[buf][kk][colx(j)]);
         b[f][j] = v.x, b[f][j + 1] = v.y, b[f][j + 2] = v.z, b[f][j + 3] = v.w;
       }
     };
@@ -146,11 +151,11 @@ __global__ void __launch_bounds__(kGT) gemm_kernel(const __grid_constant__ Gemm 
   // epilogue
 #pragma unroll
   for (int i = 0; i < TM; ++i) {
-    const int m = m0 + ty * TM + i;
+    const int m = m0 + row(i);
     if (m >= g.M) continue;
 #pragma unroll
     for (int j = 0; j < TN; ++j) {
-      const int n = n0 + tx * TN + j;
+      const int n = n0 + colx(j);
       if (n >= g.N) continue;
       float v = acc[i][j];
       if constexpr (EPI == kEpiBias || EPI == kEpiBiasRelu || EPI == kEpiHeads) {

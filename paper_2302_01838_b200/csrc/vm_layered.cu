@@ -550,6 +550,7 @@ size_t layered_train_bytes(const VmStack* stacks, const VmBatch* batches, int n,
   size_t m = 0;
   for (int i = first; i < n; ++i) {
     lyr::Plan p;
+    if (lyr::check_batch(stacks[i], batches[i])) return 0;
     if (lyr::plan(stacks[i], int64_t(batches[i].n_rays) * batches[i].n_points, batches[i].n_rays, true, true, p))
       return 0;
     m = std::max(m, p.bytes);  // stacks run one after another: one region serves all

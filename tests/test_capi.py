@@ -51,3 +51,35 @@ def test_layout_wide_models():
     assert L.hidden_pad == 224
     assert list(L.fi_pad[:4]) == [64, 224, 224, 224] and list(L.fo_pad[:4]) == [224, 224, 224, 4]
     assert L.n_params == 200 * 63 + 200 + 2 * (200 * 200 + 200) + 4 * 200 + 4
+
+
+def _plan_bytes(archs, rays, points):
+    """vm_train_workspace_bytes for stacks of the given (n_layers, hidden,
+    n_freq) architectures -- host-only planning, no device pointer is read."""
+    lib = _lib.load()
+    n = len(archs)
+    vs = (_lib.VmStack * n)()
+    vb = (_lib.VmBatch * n)()
+    for i, (nl, h, f) in enumerate(archs):
+        d = 3 + 6 * f
+        vs[i].arch = _lib.VmArch(nl, h, d, 0)
+        vs[i].count = vs[i].capacity = 2
+        vb[i].n_models, vb[i].n_rays, vb[i].n_points, vb[i].input_dim = 2, rays, points, d
+        vb[i].encoded = 16  # non-null: the layered path takes the encoded input
+    return lib.vm_train_workspace_bytes(vs, vb, n)
+
+
+def test_train_planning_routes_wide_models_to_the_layered_path():
+    """The fused plan for the config-2 stacks; the layered plan (all layer
+    activations kept for the backward: (L-1) x K x R*S x hidden_pad floats
+    and more) for widths / sample counts the fused kernels lack; the hybrid
+    (fused objects + layered background) in between."""
+    fused = _plan_bytes([(4, 32, 5), (4, 128, 5)], 120, 10)
+    assert fused > 0
+    acts = 3 * 2 * 120 * 10 * 256 * 4
+    wide = _plan_bytes([(4, 256, 5)], 120, 10)
+    assert wide > acts
+    assert _plan_bytes([(4, 64, 5)], 30, 40) > 3 * 2 * 30 * 40 * 64 * 4  # 40 samples per ray
+    hybrid = _plan_bytes([(4, 32, 5), (4, 256, 5)], 120, 10)
+    assert hybrid >= _plan_bytes([(4, 32, 5)], 120, 10) + wide
+    assert _plan_bytes([(4, 32, 5)], 120, 65) == 0  # > 64 samples per ray: rejected

@@ -216,3 +216,17 @@ def test_layered_forced_on_the_bench_architectures(cuda):
                        timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
     assert "layered ok" in r.stdout
+
+
+def test_layered_query_grid_vs_oracle(cuda):
+    """meshing.py:64-97 query_grid for a hidden-256 model (inference on the
+    layered forward, several chunks)."""
+    from paper_2302_01838_b200.geometry import AABB
+    from paper_2302_01838_b200.meshing import query_grid
+    arch = ModelArch(n_layers=4, hidden=256, n_freq=5)
+    params, _ = init_stacked(arch, 2, seed=9)
+    ost = O.new_stack(oracle_arch(arch), 2, 9)
+    box = AABB(np.array([-0.4, -0.3, -0.5]), np.array([0.5, 0.6, 0.2]))
+    g = query_grid(params, 1, box, 0.8, 24, chunk=5000)
+    exp = O.query_grid(ost, 1, box.min, box.max, 0.8, 24)
+    np.testing.assert_allclose(g.values, exp, rtol=1e-4, atol=1e-6)

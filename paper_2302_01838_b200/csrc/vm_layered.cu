@@ -51,10 +51,12 @@ struct Gemm {
   float* col;
   int64_t sO;
   int splits, kchunk; // blockIdx.z = batch * splits + split; split s reduces k in [s*kchunk, (s+1)*kchunk)
+  int db_row;         // kEpiStore, >= 0: the m0 == 0 CTAs also store the column sums of B (sum_k B(k, n),
+                      // the bias gradient) as row db_row of C, accumulated in the same k order
 };
 
 template <int BM, int BN, int TM, int TN, bool AK, bool BKc, int EPI>
-__global__ void __launch_bounds__(kGT) gemm_kernel(const __grid_constant__ Gemm g) {
+__global__ void __launch_bounds__(kGT, 2) gemm_kernel(const __grid_constant__ Gemm g) {
   static_assert((BM / TM) * (BN / TN) == kGT, "one register block per thread");
   constexpr int EA = BM * kBK / kGT, EB = BN * kBK / kGT;
   __shared__ __align__(16) float As[2][kBK][BM];
@@ -112,6 +114,12 @@ __global__ void __launch_bounds__(kGT) gemm_kernel(const __grid_constant__ Gemm 
   for (int i = 0; i < TM; ++i)
 #pragma unroll
     for (int j = 0; j < TN; ++j) acc[i][j] = 0.f;
+  // bias gradient: column sums of B, by the threads of register-block row 0
+  // of the first M tile (each column has exactly one such thread)
+  const bool dbt = EPI == kEpiStore && g.db_row >= 0 && blockIdx.y == 0 && ty == 0;
+  float dbacc[TN];
+#pragma unroll
+  for (int j = 0; j < TN; ++j) dbacc[j] = 0.f;
   int buf = 0;
   if (k_begin < k_end) {
     load(k_begin);
@@ -143,12 +151,25 @@ __global__ void __launch_bounds__(kGT) gemm_kernel(const __grid_constant__ Gemm 
       for (int i = 0; i < TM; ++i)
 #pragma unroll
         for (int j = 0; j < TN; ++j) acc[i][j] = __fmaf_rn(a[kk & 1][i], b[kk & 1][j], acc[i][j]);
+      if constexpr (EPI == kEpiStore) {
+        if (dbt) {
+#pragma unroll
+          for (int j = 0; j < TN; ++j) dbacc[j] = __fadd_rn(dbacc[j], b[kk & 1][j]);
+        }
+      }
     }
     if (more) store(buf ^ 1);
     __syncthreads();
     buf ^= 1;
   }
   // epilogue
+  if (dbt) {
+#pragma unroll
+    for (int j = 0; j < TN; ++j) {
+      const int n = n0 + colx(j);
+      if (n < g.N) g.C[batch * g.sC + split * g.sCsplit + int64_t(g.db_row) * g.ldc + n] = dbacc[j];
+    }
+  }
 #pragma unroll
   for (int i = 0; i < TM; ++i) {
     const int m = m0 + row(i);
@@ -484,25 +505,27 @@ int backward(const VmStack& st, const Plan& p, const float* enc, int D, char* ws
     const int fo_pad = p.L.fo_pad[l], fi_pad = p.L.fi_pad[l];
     const float* x = l == 0 ? enc : act + size_t(l - 1) * K * N * hp;
     const int64_t ldx = l == 0 ? D : hp;
-    // [dW^T ; db] = [x | 1]^T dz, split over samples
+    // [dW^T ; db] = [x | 1]^T dz, split over samples (the ones row, db, as
+    // the column sums of dz inside the same launch: no extra M tile)
     Gemm g{};
-    g.M = fi_pad + 1;
+    g.M = fi_pad;
     g.N = fo_pad;
     g.Kd = int(N);
     g.A = x, g.lda = ldx, g.sA = N * ldx;
     g.a_valid = l == 0 ? D : int(hp);
-    g.a_ones = fi_pad;
+    g.a_ones = -1;
+    g.db_row = fi_pad;
     g.B = dzb[cur], g.ldb = fo_pad, g.sB = N * fo_pad;
-    g.splits = dw_splits(N, g.M, g.N);
+    g.splits = dw_splits(N, fi_pad + 1, g.N);
     g.kchunk = dw_chunk(N, g.splits);
-    g.C = part, g.ldc = g.N, g.sCsplit = int64_t(g.M) * g.N, g.sC = g.splits * g.sCsplit;
+    g.C = part, g.ldc = g.N, g.sCsplit = int64_t(fi_pad + 1) * g.N, g.sC = g.splits * g.sCsplit;
     int rc = launch_gemm<kEpiStore, false, false>(g, K, s);
     if (rc) return rc;
     ReduceArgs r{};
-    r.M = g.M, r.N = g.N, r.splits = g.splits, r.fi_pad = fi_pad;
+    r.M = fi_pad + 1, r.N = g.N, r.splits = g.splits, r.fi_pad = fi_pad;
     r.part = part, r.grads = grads, r.block = p.L.block, r.w_off = p.L.w_off[l], r.b_off = p.L.b_off[l];
     r.upd = upd, r.status = status;
-    const int64_t MN = int64_t(g.M) * g.N;
+    const int64_t MN = int64_t(r.M) * g.N;
     reduce_kernel<<<dim3(unsigned((MN + 255) / 256), K), 256, 0, s>>>(r);
     VM_CUDA(cudaGetLastError());
     if (l == 0) break;

@@ -52,7 +52,8 @@ struct Gemm {
   int64_t sO;
   int splits, kchunk; // blockIdx.z = batch * splits + split; split s reduces k in [s*kchunk, (s+1)*kchunk)
   int db_row;         // kEpiStore, >= 0: the m0 == 0 CTAs also store the column sums of B (sum_k B(k, n),
-                      // the bias gradient) as row db_row of C, accumulated in the same k order
+                      // the bias gradient) as element db_row of C^T's row n, accumulated in the same k order
+                      // (kEpiStore writes C transposed: C^T[n*ldc + m], ldc % 4 == 0)
 };
 
 template <int BM, int BN, int TM, int TN, bool AK, bool BKc, int EPI>
@@ -163,15 +164,37 @@ __global__ void __launch_bounds__(kGT, 2) gemm_kernel(const __grid_constant__ Ge
     buf ^= 1;
   }
   // epilogue
+  if constexpr (EPI == kEpiStore) {
+    // weight-gradient partials as C^T (output-major, the arena's dW row
+    // order): four consecutive m of one n per float4
+    float* C = g.C + batch * g.sC + split * g.sCsplit;
+#pragma unroll
+    for (int i = 0; i < TM; i += 4) {
+      const int m = m0 + row(i);
+#pragma unroll
+      for (int j = 0; j < TN; ++j) {
+        const int n = n0 + colx(j);
+        if (n >= g.N) continue;
+        if (m + 3 < g.M) {
+          st4(C + int64_t(n) * g.ldc + m, make_float4(acc[i][j], acc[i + 1][j], acc[i + 2][j], acc[i + 3][j]));
+        } else {
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (m + u < g.M) C[int64_t(n) * g.ldc + m + u] = acc[i + u][j];
+        }
+      }
+    }
+  }
   if (dbt) {
 #pragma unroll
     for (int j = 0; j < TN; ++j) {
       const int n = n0 + colx(j);
-      if (n < g.N) g.C[batch * g.sC + split * g.sCsplit + int64_t(g.db_row) * g.ldc + n] = dbacc[j];
+      if (n < g.N) g.C[batch * g.sC + split * g.sCsplit + int64_t(n) * g.ldc + g.db_row] = dbacc[j];
     }
   }
 #pragma unroll
   for (int i = 0; i < TM; ++i) {
+    if constexpr (EPI == kEpiStore) break;
     const int m = m0 + row(i);
     if (m >= g.M) continue;
 #pragma unroll
@@ -322,7 +345,8 @@ __global__ void __launch_bounds__(128) meta_kernel(const __grid_constant__ MetaA
 }
 
 struct ReduceArgs {
-  int M, N, splits;       // partial blocks [splits][M][N] per model (M = fi_pad + 1: last row = db)
+  int M, N, splits;       // partial blocks [splits][N][ldp] per model (C^T; M = fi_pad + 1: element fi_pad = db)
+  int ldp;
   int fi_pad;
   const float* part;
   float* grads;           // [K][block]
@@ -339,13 +363,15 @@ __global__ void __launch_bounds__(256) reduce_kernel(const __grid_constant__ Red
   const int k = blockIdx.y;
   const int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   const int64_t MN = int64_t(a.M) * a.N;
+  const int64_t blk = int64_t(a.ldp) * a.N;  // one sample chunk's partial block
   bool bad = false;
   if (e < MN) {
-    // e enumerates the destination: output o = e / M (row of dW), input i = e % M
+    // e enumerates output o = e / M (row of dW) and input i = e % M, in the
+    // order of both the partials (C^T rows of ldp floats) and the arena
     const int o = int(e / a.M), i = int(e % a.M);
-    const float* p = a.part + int64_t(k) * a.splits * MN + int64_t(i) * a.N + o;
+    const float* p = a.part + int64_t(k) * a.splits * blk + int64_t(o) * a.ldp + i;
     float v = p[0];
-    for (int s = 1; s < a.splits; ++s) v = __fadd_rn(v, p[s * MN]);
+    for (int s = 1; s < a.splits; ++s) v = __fadd_rn(v, p[s * blk]);
     float* gk = a.grads + int64_t(k) * a.block;
     if (i == a.fi_pad) gk[a.b_off + o] = v;
     else gk[a.w_off + int64_t(o) * a.fi_pad + i] = v;
@@ -439,7 +465,7 @@ int plan(const VmStack& st, int64_t n_samples, int R, bool train, bool keep_acts
   if (keep_acts)
     for (int l = 0; l < nl; ++l) {
       const int M = p.L.fi_pad[l] + 1, Nn = p.L.fo_pad[l];
-      p.part_floats = std::max(p.part_floats, size_t(dw_splits(n_samples, M, Nn)) * M * Nn);
+      p.part_floats = std::max(p.part_floats, size_t(dw_splits(n_samples, M, Nn)) * (M + 3) * Nn);
     }
   p.off_part = off;  off = al(off + K * p.part_floats * 4);
   p.off_grads = off; off = al(off + (train ? K * size_t(p.L.block) * 4 : 0));
@@ -518,11 +544,11 @@ int backward(const VmStack& st, const Plan& p, const float* enc, int D, char* ws
     g.B = dzb[cur], g.ldb = fo_pad, g.sB = N * fo_pad;
     g.splits = dw_splits(N, fi_pad + 1, g.N);
     g.kchunk = dw_chunk(N, g.splits);
-    g.C = part, g.ldc = g.N, g.sCsplit = int64_t(fi_pad + 1) * g.N, g.sC = g.splits * g.sCsplit;
+    g.C = part, g.ldc = fi_pad + 4, g.sCsplit = int64_t(fi_pad + 4) * g.N, g.sC = g.splits * g.sCsplit;
     int rc = launch_gemm<kEpiStore, false, false>(g, K, s);
     if (rc) return rc;
     ReduceArgs r{};
-    r.M = fi_pad + 1, r.N = g.N, r.splits = g.splits, r.fi_pad = fi_pad;
+    r.M = fi_pad + 1, r.N = g.N, r.ldp = fi_pad + 4, r.splits = g.splits, r.fi_pad = fi_pad;
     r.part = part, r.grads = grads, r.block = p.L.block, r.w_off = p.L.w_off[l], r.b_off = p.L.b_off[l];
     r.upd = upd, r.status = status;
     const int64_t MN = int64_t(r.M) * g.N;

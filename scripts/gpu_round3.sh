@@ -2,7 +2,7 @@
 # Final measurement set without full ncu captures (<64 MiB of outputs): tests, smoke, bench (config 2 +
 # CPU baseline), reference arm, configs 3/4, ncu launch list, sweep, sanitizers.
 mkdir -p gpurun_out
-T=${TAG:-r02j}
+T=${TAG:-r02k}
 timeout 1500 python -m pytest tests -m gpu -q -rf > gpurun_out/${T}_pytest.log 2>&1; echo "pytest rc=$?"; tail -2 gpurun_out/${T}_pytest.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${T}_smoke.log 2>&1; echo "smoke rc=$?"; tail -1 gpurun_out/${T}_smoke.log
 timeout 600 python bench.py --impl reference --steps 20 --warmup 5 > gpurun_out/${T}_bench_reference.json 2> gpurun_out/ref.err; echo "ref rc=$?"

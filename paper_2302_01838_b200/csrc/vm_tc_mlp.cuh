@@ -232,8 +232,8 @@ struct Smem {
   static constexpr int coef = tr + kTM * 4;                  // 8 PE coefficients
   static constexpr int tgt = coef + 8 * 4;                   // [kTM rays][8] targets (depth, rgb, flags)
   static constexpr int db = tgt + kTM * 8 * 4;               // kCW warps x kDbW
-  static constexpr int bars = (db + kCW * kDbW * 4 + 7) / 8 * 8;  // 3*kNS + 1 u64
-  static constexpr int tmem = bars + (3 * kNS + 1) * 8;
+  static constexpr int bars = (db + kCW * kDbW * 4 + 7) / 8 * 8;  // 3*kNS + 2 u64
+  static constexpr int tmem = bars + (3 * kNS + 2) * 8;
   static constexpr int chunks = tmem + 16;                     // schedule table (MMA warp)
   static constexpr int total = chunks + 64 * 36;
 };
@@ -249,6 +249,8 @@ struct Chunk {
   int first, last;
   int w_off;   // weight-image offset (floats) of the B half, -1: B staged by the compute warps
   int w_floats;
+  int dst = 0;  // TMEM accumulator column (KT backward: dW_l into the region G_l was read from)
+  int acc = 0;  // accumulator barrier the last chunk commits to (1: KT's dx GEMMs)
 };
 
 template <int H, int L, class F>
@@ -261,11 +263,14 @@ __device__ __forceinline__ void for_each_chunk(F&& f) {
     for (int c = 0; c < H / 32; ++c)
       f(j++, Chunk{0, 32, 4, H, 0, c == 0, c == H / 32 - 1, I::fwd_off(l) + c * I::kC32, I::kC32});
   for (int c = 0; c < 4; ++c) f(j++, Chunk{2, 32, 4, 16, H, c == 0, c == 3, -1, 0});
+  // backward, per hidden layer l: dW_l (into TMEM region l+1, which held G_l)
+  // then dx_l (into region 0, on its own accumulator barrier), so the two
+  // GEMMs run back to back while the compute warps drain dW_l
   for (int l = L - 2; l >= 0; --l) {
-    for (int c = 0; c < 4; ++c) f(j++, Chunk{2, 32, 4, H, H, c == 0, c == 3, -1, 0});
+    for (int c = 0; c < 4; ++c) f(j++, Chunk{2, 32, 4, H, H, c == 0, c == 3, -1, 0, (l + 1) * H, 0});
     if (l > 0)
       for (int c = 0; c < H / 32; ++c)
-        f(j++, Chunk{0, 32, 4, H, 0, c == 0, c == H / 32 - 1, I::dx_off(l) + c * I::kC32, I::kC32});
+        f(j++, Chunk{0, 32, 4, H, 0, c == 0, c == H / 32 - 1, I::dx_off(l) + c * I::kC32, I::kC32, 0, 1});
   }
 }
 
@@ -303,7 +308,7 @@ __global__ void __launch_bounds__(kTCThreads, 1)
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + SM::bars);
   uint64_t* empty = full + kNS;
   uint64_t* wfull = empty + kNS;
-  uint64_t* accf = wfull + kNS;
+  uint64_t* accf = wfull + kNS;  // [2]: layer/dW accumulators, dx accumulators
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + SM::tmem);
 
   if (warp == 0) tc::tmem_alloc(tmem_slot, 512);
@@ -313,7 +318,8 @@ __global__ void __launch_bounds__(kTCThreads, 1)
       tc::mbar_init(&empty[s], 1);
       tc::mbar_init(&wfull[s], 1);
     }
-    tc::mbar_init(accf, 1);
+    tc::mbar_init(&accf[0], 1);
+    tc::mbar_init(&accf[1], 1);
     tc::mbar_fence_init();
   }
   for (int l = 0; l < L - 1; ++l)
@@ -370,6 +376,7 @@ __global__ void __launch_bounds__(kTCThreads, 1)
         tc::fence_after_sync();
         const uint32_t sa = tc::smem_u32(smem + s * kSlot);
         const uint32_t idesc = tc::idesc_tf32(128, ci.n, false, false);
+        const uint32_t tmd = tm + uint32_t(ci.dst);
         if (!ci.sw) {
           const int kw = ci.kw;
           const uint32_t a_lo = sa + kTM * kw * 4, b_hi = sa + kHalfSlot, b_lo = b_hi + ci.n * kw * 4;
@@ -377,10 +384,10 @@ __global__ void __launch_bounds__(kTCThreads, 1)
             const uint32_t o = ks * 256;
             const uint64_t ah = tc::sdesc(sa + o, 128, kw * 32), al = tc::sdesc(a_lo + o, 128, kw * 32);
             const uint64_t bh = tc::sdesc(b_hi + o, 128, kw * 32), bl = tc::sdesc(b_lo + o, 128, kw * 32);
-            tc::mma_tf32(tm, al, bh, idesc, (ci.first && ks == 0) ? 0u : 1u);
-            tc::mma_tf32(tm, ah, bl, idesc, 1u);
-            tc::mma_tf32(tm, ah, bh, idesc, 1u);
-            if (VM_KT_PRODUCTS > 3) tc::mma_tf32(tm, al, bl, idesc, 1u);
+            tc::mma_tf32(tmd, al, bh, idesc, (ci.first && ks == 0) ? 0u : 1u);
+            tc::mma_tf32(tmd, ah, bl, idesc, 1u);
+            tc::mma_tf32(tmd, ah, bh, idesc, 1u);
+            if (VM_KT_PRODUCTS > 3) tc::mma_tf32(tmd, al, bl, idesc, 1u);
           }
         } else if (ci.sw == 2) {
           const uint32_t idesc_mn = tc::idesc_tf32(128, ci.n, true, true);
@@ -389,10 +396,10 @@ __global__ void __launch_bounds__(kTCThreads, 1)
             const uint32_t o = ks * 1024;
             const uint64_t ah = sdesc_mn(sa + o), al = sdesc_mn(a_lo + o);
             const uint64_t bh = sdesc_mn(b_hi + o), bl = sdesc_mn(b_lo + o);
-            tc::mma_tf32(tm, al, bh, idesc_mn, (ci.first && ks == 0) ? 0u : 1u);
-            tc::mma_tf32(tm, ah, bl, idesc_mn, 1u);
-            tc::mma_tf32(tm, ah, bh, idesc_mn, 1u);
-            if (VM_KT_PRODUCTS > 3) tc::mma_tf32(tm, al, bl, idesc_mn, 1u);
+            tc::mma_tf32(tmd, al, bh, idesc_mn, (ci.first && ks == 0) ? 0u : 1u);
+            tc::mma_tf32(tmd, ah, bl, idesc_mn, 1u);
+            tc::mma_tf32(tmd, ah, bh, idesc_mn, 1u);
+            if (VM_KT_PRODUCTS > 3) tc::mma_tf32(tmd, al, bl, idesc_mn, 1u);
           }
         } else {
           const uint32_t a_lo = sa + ci.m_rows * 128, b_hi = sa + kHalfSlot, b_lo = b_hi + ci.n * 128;
@@ -400,14 +407,14 @@ __global__ void __launch_bounds__(kTCThreads, 1)
             const uint32_t o = ks * 32;
             const uint64_t ah = sdesc_sw128(sa + o), al = sdesc_sw128(a_lo + o);
             const uint64_t bh = sdesc_sw128(b_hi + o), bl = sdesc_sw128(b_lo + o);
-            tc::mma_tf32(tm, al, bh, idesc, (ci.first && ks == 0) ? 0u : 1u);
-            tc::mma_tf32(tm, ah, bl, idesc, 1u);
-            tc::mma_tf32(tm, ah, bh, idesc, 1u);
-            if (VM_KT_PRODUCTS > 3) tc::mma_tf32(tm, al, bl, idesc, 1u);
+            tc::mma_tf32(tmd, al, bh, idesc, (ci.first && ks == 0) ? 0u : 1u);
+            tc::mma_tf32(tmd, ah, bl, idesc, 1u);
+            tc::mma_tf32(tmd, ah, bh, idesc, 1u);
+            if (VM_KT_PRODUCTS > 3) tc::mma_tf32(tmd, al, bl, idesc, 1u);
           }
         }
         tc::mma_commit(&empty[s]);
-        if (ci.last) tc::mma_commit(accf);
+        if (ci.last) tc::mma_commit(&accf[ci.acc]);
       }
     }
     __syncwarp();
@@ -419,7 +426,7 @@ __global__ void __launch_bounds__(kTCThreads, 1)
     const uint32_t tq = tm + (uint32_t(32 * q) << 16);      // this warp's lane quadrant
     auto R = [&](int j) { return tq + uint32_t(j * H); };   // TMEM region j (column base)
     float* myDb = sDb + warp * SM::kDbW;
-    uint32_t it = 0, accn = 0;
+    uint32_t it = 0, accn[2] = {0, 0};
     auto acquire = [&]() -> uint8_t* {
       const uint32_t s = it % kNS;
       if (it >= uint32_t(kNS)) tc::mbar_wait(&empty[s], ((it / kNS) - 1) & 1);
@@ -448,13 +455,13 @@ __global__ void __launch_bounds__(kTCThreads, 1)
       tc::mbar_arrive(&full[it % kNS]);
       ++it;
     };
-    auto wait_acc = [&]() {
+    auto wait_acc = [&](int a = 0) {  // a = 1: the dx accumulator
       VM_TC_T(vm_ev);
 #ifdef VM_TC_DEBUG
       ++vm_ev;
 #endif
-      tc::mbar_wait(accf, accn & 1);
-      ++accn;
+      tc::mbar_wait(&accf[a], accn[a] & 1);
+      ++accn[a];
       tc::fence_after_sync();
       VM_TC_T(vm_ev);
 #ifdef VM_TC_DEBUG
@@ -741,20 +748,19 @@ __global__ void __launch_bounds__(kTCThreads, 1)
       // writes its own sample's features as float4s), so TMEM lane = fan-in
       // and the drain writes whole 128-B rows of the gradient; layer 0 (fan-in
       // 33) keeps K-major transposed tiles with A = G_0^T (M = fan-out).
+      // Every thread reads its G_l row (owned columns) from TMEM region l+1
+      // before its first release: dW_l accumulates into that region, and the
+      // row stays in registers for the dx_l operand and the bias gradient.
+      float gv[2][32];
+      ld64(R(l + 1) + c0, R(l + 1) + c0 + 32, gv[0], gv[1]);
 #pragma unroll 1
       for (int c = 0; c < 4; ++c) {
         uint8_t* sl = acquire();
         if (q == c) {
           uint8_t* gt = sl + kHalfSlot;  // B = G_l (N = fan-out)
           uint8_t* xt = sl;              // A = X_l (M = fan-in; layer 0 zero-padded to 128)
-          float gv2[2][32];
-          ld64(R(l + 1) + c0, R(l + 1) + c0 + 32, gv2[0], gv2[1]);
-#pragma unroll
-          for (int g = 0; g < 2; ++g) {
-            float (&v)[32] = gv2[g];
-            put_mn(gt, c0 + 32 * g, v);
-            myDb[l * H + c0 + 32 * g + lane] += warp_colsum(v);
-          }
+          put_mn(gt, c0, gv[0]);
+          put_mn(gt, c0 + 32, gv[1]);
           if (l == 0) {
             // last weight-gradient GEMM of the tile: let the partial-reduce
             // grid (launched programmatically behind this one) be scheduled
@@ -786,27 +792,10 @@ __global__ void __launch_bounds__(kTCThreads, 1)
         }
         release();
       }
-      wait_acc();
-      {  // drain dW_l^T: lane = fan-in i, columns = this half's fan-out rows
-        const int i = row;
-        const int fi_pad = (l == 0) ? st.fi0 : H;  // layer 0: fan-in rows >= 36 do not exist
-        float* dst = gdst + st.w_off[l] + i;
-#pragma unroll
-        for (int cc = 0; cc < HC; cc += 16) {
-          float v[16];
-          tc::tmem_ld16(R(0) + c0 + cc, v);  // warp-wide (.sync.aligned): no divergence before it
-          if (i < fi_pad) {
-#pragma unroll
-            for (int j = 0; j < 16; ++j) dst[(c0 + cc + j) * fi_pad] = v[j];
-          }
-        }
-      }
-      if (l == 0) break;
       // G_{l-1} = (G_l W_l) * (X_l > 0): A = G_l rows (chunk c by the half
-      // owning those columns), B = W_l^T chunks (TMA)
-      {
-        float gv[2][32];
-        ld64(R(l + 1) + c0, R(l + 1) + c0 + 32, gv[0], gv[1]);
+      // owning those columns), B = W_l^T chunks (TMA); issued right behind
+      // dW_l, into region 0 on the dx barrier
+      if (l > 0) {
 #pragma unroll 1
         for (int c = 0; c < H / 32; ++c) {
           uint8_t* sl = acquire_w(I::dx_off(l) + c * I::kC32, I::kC32, c >> 1);
@@ -819,7 +808,27 @@ __global__ void __launch_bounds__(kTCThreads, 1)
           release();
         }
       }
+      // bias gradient db_l: column sums of G_l over the warp's 32 rows (while
+      // the tensor core runs dW_l / dx_l)
+#pragma unroll
+      for (int g = 0; g < 2; ++g) myDb[l * H + c0 + 32 * g + lane] += warp_colsum(gv[g]);
       wait_acc();
+      {  // drain dW_l^T from region l+1: lane = fan-in i, columns = this half's fan-out rows
+        const int i = row;
+        const int fi_pad = (l == 0) ? st.fi0 : H;  // layer 0: fan-in rows >= 36 do not exist
+        float* dst = gdst + st.w_off[l] + i;
+#pragma unroll
+        for (int cc = 0; cc < HC; cc += 16) {
+          float v[16];
+          tc::tmem_ld16(R(l + 1) + c0 + cc, v);  // warp-wide (.sync.aligned): no divergence before it
+          if (i < fi_pad) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) dst[(c0 + cc + j) * fi_pad] = v[j];
+          }
+        }
+      }
+      if (l == 0) break;
+      wait_acc(1);
 #pragma unroll
       for (int g = 0; g < 2; ++g) {
         float d[32], a[32];

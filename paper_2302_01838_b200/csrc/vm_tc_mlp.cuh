@@ -262,7 +262,8 @@ __device__ __forceinline__ void for_each_chunk(F&& f) {
   for (int l = 1; l <= L - 2; ++l)
     for (int c = 0; c < H / 32; ++c)
       f(j++, Chunk{0, 32, 4, H, 0, c == 0, c == H / 32 - 1, I::fwd_off(l) + c * I::kC32, I::kC32});
-  for (int c = 0; c < 4; ++c) f(j++, Chunk{2, 32, 4, 16, H, c == 0, c == 3, -1, 0});
+  // output layer dW3 (N = 16) on the dx barrier: drained while dW_{L-2} runs
+  for (int c = 0; c < 4; ++c) f(j++, Chunk{2, 32, 4, 16, H, c == 0, c == 3, -1, 0, 0, 1});
   // backward, per hidden layer l: dW_l (into TMEM region l+1, which held G_l)
   // then dx_l (into region 0, on its own accumulator barrier), so the two
   // GEMMs run back to back while the compute warps drain dW_l
@@ -695,7 +696,10 @@ __global__ void __launch_bounds__(kTCThreads, 1)
 
     // ---------------------------------------------------------- backward
     // output layer: dW3^T = X3^T G3 (MMA, M = H, N = 16), db3, and
-    // G2 = (G3 W3) * (X3 > 0) written over X3 in TMEM (owned columns).
+    // G2 = (G3 W3) * (X3 > 0) kept in registers (owned columns).  G_l rows
+    // stay in registers from here on: each dx epilogue produces the next
+    // (dW_{l-1} accumulates over TMEM region l, so nothing is stored back).
+    float gv[2][32];
 #pragma unroll 1
     for (int c = 0; c < 4; ++c) {
       uint8_t* sl = acquire();
@@ -710,16 +714,14 @@ __global__ void __launch_bounds__(kTCThreads, 1)
           for (int j = 0; j < 32; ++j) {
             const float4 w = ld4(sW3t + 4 * (c0 + 32 * g + j));
             const float a = fmaf(g3[3], w.w, fmaf(g3[2], w.z, fmaf(g3[1], w.y, g3[0] * w.x)));
-            v[j] = v[j] > 0.f ? a : 0.f;
+            gv[g][j] = v[j] > 0.f ? a : 0.f;
           }
-          st32(R(L - 1) + c0 + 32 * g, v);
         }
-        tc::tmem_st_wait();
         if (h == 0) {
-          float gv[32];
+          float gb[32];
 #pragma unroll
-          for (int o = 0; o < 32; ++o) gv[o] = o < 4 ? g3[o < 4 ? o : 0] : 0.f;
-          put_mn(sl + kHalfSlot, 0, gv);  // B = G3 (N = 16, 4 live)
+          for (int o = 0; o < 32; ++o) gb[o] = o < 4 ? g3[o < 4 ? o : 0] : 0.f;
+          put_mn(sl + kHalfSlot, 0, gb);  // B = G3 (N = 16, 4 live)
 #pragma unroll
           for (int o = 0; o < 4; ++o) {
             float a = g3[o];
@@ -731,14 +733,6 @@ __global__ void __launch_bounds__(kTCThreads, 1)
       }
       release();
     }
-    wait_acc();
-    if (h == 0) {
-      float v[16];
-      tc::tmem_ld16(R(0), v);
-      const int i = row;  // lane = fan-in index
-#pragma unroll
-      for (int o = 0; o < 4; ++o) gdst[st.w_off[L - 1] + o * H + i] = v[o];
-    }
 
 #pragma unroll 1
     for (int l = L - 2; l >= 0; --l) {
@@ -748,11 +742,9 @@ __global__ void __launch_bounds__(kTCThreads, 1)
       // writes its own sample's features as float4s), so TMEM lane = fan-in
       // and the drain writes whole 128-B rows of the gradient; layer 0 (fan-in
       // 33) keeps K-major transposed tiles with A = G_0^T (M = fan-out).
-      // Every thread reads its G_l row (owned columns) from TMEM region l+1
-      // before its first release: dW_l accumulates into that region, and the
-      // row stays in registers for the dx_l operand and the bias gradient.
-      float gv[2][32];
-      ld64(R(l + 1) + c0, R(l + 1) + c0 + 32, gv[0], gv[1]);
+      // Every thread holds its G_l row (owned columns) in registers before
+      // its first release: dW_l accumulates into TMEM region l+1, and the row
+      // feeds the dx_l operand and the bias gradient.
 #pragma unroll 1
       for (int c = 0; c < 4; ++c) {
         uint8_t* sl = acquire();
@@ -792,6 +784,16 @@ __global__ void __launch_bounds__(kTCThreads, 1)
         }
         release();
       }
+      if (l == L - 2) {  // dW3^T (region 0, dx barrier): drained before dx_l reuses region 0
+        wait_acc(1);
+        if (h == 0) {
+          float v[16];
+          tc::tmem_ld16(R(0), v);
+          const int i = row;  // lane = fan-in index
+#pragma unroll
+          for (int o = 0; o < 4; ++o) gdst[st.w_off[L - 1] + o * H + i] = v[o];
+        }
+      }
       // G_{l-1} = (G_l W_l) * (X_l > 0): A = G_l rows (chunk c by the half
       // owning those columns), B = W_l^T chunks (TMA); issued right behind
       // dW_l, into region 0 on the dx barrier
@@ -829,15 +831,14 @@ __global__ void __launch_bounds__(kTCThreads, 1)
       }
       if (l == 0) break;
       wait_acc(1);
+      // G_{l-1} = dx * (X_l > 0), kept in registers for the next layer
 #pragma unroll
       for (int g = 0; g < 2; ++g) {
-        float d[32], a[32];
-        ld64(R(0) + c0 + 32 * g, R(l) + c0 + 32 * g, d, a);
+        float a[32];
+        ld64(R(0) + c0 + 32 * g, R(l) + c0 + 32 * g, gv[g], a);
 #pragma unroll
-        for (int j = 0; j < 32; ++j) d[j] = a[j] > 0.f ? d[j] : 0.f;
-        st32(R(l) + c0 + 32 * g, d);
+        for (int j = 0; j < 32; ++j) gv[g][j] = a[j] > 0.f ? gv[g][j] : 0.f;
       }
-      tc::tmem_st_wait();
     }
     compute_sync();
     VM_TC_T(vm_ev);

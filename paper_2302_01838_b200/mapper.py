@@ -531,27 +531,44 @@ class Mapper:
             st = host[3 * n:].reshape(-1, 4)
         else:
             stacks = []
-        row = 0
         w = self.cfg.loss_weights
         wc, wo = w.colour, w.occupancy
         total = 0
-        for si, (params, _, _) in enumerate(stacks):
-            is_bg = params is self.bg_params
-            kk = params.count
-            if st[si, 0] < kk:
-                raise FloatingPointError(f"non-finite gradient for model index {int(st[si, 0])}")
-            vals = l[row:row + kk]
-            ids = [0] if is_bg else self.model_to_object
-            if st[si, 1] < kk or not np.isfinite(vals).all():
-                bad = int(np.flatnonzero(~np.isfinite(vals).all(axis=1))[0])
-                raise FloatingPointError(f"non-finite loss for object {ids[bad]}")
-            rows = vals.astype(np.float64).tolist()
-            report_losses.update(zip(ids, map(tuple, rows)))
-            row += kk
-            k_models += kk
-        # the reference's sum over report.losses.values() in insertion order
-        for d, c, o in report_losses.values():
-            total += d + wc * c + wo * o
+        counts = [params.count for params, _, _ in stacks]
+        n_rows = sum(counts)
+        v64 = l[:n_rows].astype(np.float64) if stacks else None
+        fast = not stacks or (all(st[si, 0] >= kk and st[si, 1] >= kk for si, kk in enumerate(counts))
+                              and bool(np.isfinite(v64).all()))
+        if not stacks:
+            pass
+        elif fast:
+            # one conversion for every model's row, no per-stack Python loop
+            ids = []
+            for params, _, _ in stacks:
+                ids.extend([0] if params is self.bg_params else self.model_to_object[:params.count])
+            report_losses = dict(zip(ids, map(tuple, v64.tolist())))
+            k_models = n_rows
+            if len(report_losses) == n_rows and n_rows:
+                # the reference's left-to-right sum over report.losses.values()
+                # (np.add.accumulate is sequential; same f64 operations and order)
+                total = np.add.accumulate(v64[:, 0] + wc * v64[:, 1] + wo * v64[:, 2])[-1]
+            else:
+                for d, c, o in report_losses.values():
+                    total += d + wc * c + wo * o
+        else:  # a status word or a loss is bad: raise the reference's error, in stack order
+            row = 0
+            for si, (params, _, _) in enumerate(stacks):
+                is_bg = params is self.bg_params
+                kk = params.count
+                if st[si, 0] < kk:
+                    raise FloatingPointError(f"non-finite gradient for model index {int(st[si, 0])}")
+                vals = l[row:row + kk]
+                ids = [0] if is_bg else self.model_to_object
+                if st[si, 1] < kk or not np.isfinite(vals).all():
+                    bad = int(np.flatnonzero(~np.isfinite(vals).all(axis=1))[0])
+                    raise FloatingPointError(f"non-finite loss for object {ids[bad]}")
+                row += kk
+            raise FloatingPointError("non-finite loss")
         self.global_step += 1
         return StepReport(step=step, frame_id=self.last_frame_id, k_models=k_models, losses=report_losses,
                           total=float(total), ms=(time.perf_counter() - t0) * 1e3)

@@ -113,3 +113,24 @@ def test_sharded_shard_matches_oracle_shard(cuda):
                 np.testing.assert_allclose(np.array(rep.losses[oid]), np.array(trip), rtol=1e-4, atol=1e-5)
         if m.obj_params.count:  # the background's rank may own no objects
             assert_params_close(m.obj_params, ms.obj)
+
+
+def test_report_total_and_nonfinite_errors(cuda):
+    """StepReport.total is the reference's left-to-right sum over
+    report.losses.values() (trainer.py:395-400); a non-finite model raises
+    FloatingPointError through the graph-replayed step."""
+    scene = config("1")
+    cfg = TrainConfig()
+    m = Mapper(scene["intrinsics"], cfg)
+    populate(m, scene)
+    for _ in range(3):
+        rep = m.train_step()
+        w = cfg.loss_weights
+        total = 0
+        for d, c, o in rep.losses.values():
+            total += d + w.colour * c + w.occupancy * o
+        assert rep.total == float(total)
+        assert rep.k_models == len(rep.losses)
+    m.obj_params.arena[2].fill_(float("nan"))
+    with pytest.raises(FloatingPointError, match="non-finite"):
+        m.train_step()

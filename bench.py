@@ -43,6 +43,30 @@ UNIT = "object-steps/s"
 OBJ_PER_RANK = 50
 
 
+def kt_alone_ms(rays: int, points: int, reps: int = 20) -> float:
+    """Device time of one background-only train call (KT's weight-image prep,
+    KT, partial reduce, Adam) on an otherwise idle GPU: a config-2-shaped
+    hidden-128 model on a synthetic batch (trainer.py:594-606), launches
+    back to back between two CUDA events after a warm-up."""
+    import torch
+    from paper_2302_01838_b200 import LossWeights, ModelArch, init_stacked
+    from paper_2302_01838_b200.trainer import TrainWorkspace, _synthetic_batch, launch_train
+    ab = ModelArch(hidden=128)
+    pb, sb = init_stacked(ab, 1, seed=0, stream=2)
+    bb = _synthetic_batch(ab, 1, rays, points, seed=4)
+    ws = TrainWorkspace()
+    for _ in range(5):
+        launch_train([(pb, sb, bb)], LossWeights(), ws)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        launch_train([(pb, sb, bb)], LossWeights(), ws)
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps
+
+
 def flop_per_sample(hidden: int, input_dim: int = 33) -> int:
     """Algorithmic GEMM FLOPs per sample: 2*(2*MAC_fwd + MAC_dx)."""
     mac_fwd = hidden * input_dim + 2 * hidden * hidden + 4 * hidden
@@ -499,8 +523,17 @@ def main():
         kernels.append({"bound": "tensor", "achieved": a, "peak": tf32_peak, "unit": "TFLOP/s", "frac": a / tf32_peak,
                         "traffic": traffic_tc, "kernel": "tc_train_kernel (KT, tcgen05 3xTF32, hidden-128 background)",
                         "kernel_ms": per_tag[2], "flop_per_launch": flop_bg,
-                        "note": "3xTF32 issues 3 MMAs per algorithmic product; tensor-pipe FLOPs = 3x achieved",
+                        "note": "3xTF32 issues 3 MMAs per algorithmic product; tensor-pipe FLOPs = 3x achieved; "
+                                "kernel_ms is the branch's event span inside the step, which includes waiting "
+                                "for KF32 to free whole SMs",
                         "peak_source": tf32_src})
+        try:  # the same background stack alone on an idle GPU (prep + KT + reduce + Adam)
+            alone = kt_alone_ms(cfg.rays_background, cfg.points_per_ray)
+            kernels[-1]["alone_call_ms"] = alone
+            kernels[-1]["alone_frac"] = flop_bg / (alone * 1e-3) / 1e12 / tf32_peak
+        except Exception as e:  # measurement aid only: never fail the bench line on it
+            kernels[-1]["alone_call_ms"] = None
+            kernels[-1]["alone_error"] = repr(e)[:200]
     if not kernels:  # single FFMA launch (e.g. VM_TC=0): the phase is the kernel
         a = flop_launch / (kernel_ms * 1e-3) / 1e12
         kernels.append({"bound": "fp32", "achieved": a, "peak": ffma_peak, "unit": "TFLOP/s", "frac": a / ffma_peak,

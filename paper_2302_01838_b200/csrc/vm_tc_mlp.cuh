@@ -489,9 +489,9 @@ __global__ void __launch_bounds__(kTCThreads, 1)
     };
     // element (tile row i, sample lane) of a transposed 128B-swizzled hi/lo tile
     // 32 features [f0, f0+32) of this lane's sample into an MN-major hi/lo tile
-    auto put_mn = [&](uint8_t* t, int f0, const float (&v)[32]) {
+    auto put_mn = [&](uint8_t* t, int f0, const float (&v)[32], int nq = 8) {  // nq float4 quads (compile-time)
 #pragma unroll
-      for (int m = 0; m < 8; ++m) {
+      for (int m = 0; m < nq; ++m) {
         float4 a, b;
         split_fast(v[4 * m + 0], a.x, b.x);
         split_fast(v[4 * m + 1], a.y, b.y);
@@ -721,7 +721,7 @@ __global__ void __launch_bounds__(kTCThreads, 1)
           float gb[32];
 #pragma unroll
           for (int o = 0; o < 32; ++o) gb[o] = o < 4 ? g3[o < 4 ? o : 0] : 0.f;
-          put_mn(sl + kHalfSlot, 0, gb);  // B = G3 (N = 16, 4 live)
+          put_mn(sl + kHalfSlot, 0, gb, 4);  // B = G3: the MMA reads N = 16 columns (4 live)
 #pragma unroll
           for (int o = 0; o < 4; ++o) {
             float a = g3[o];

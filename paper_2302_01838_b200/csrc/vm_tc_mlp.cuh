@@ -758,10 +758,12 @@ __global__ void __launch_bounds__(kTCThreads, 1)
             // grid (launched programmatically behind this one) be scheduled
             // now; it waits on griddepcontrol.wait for this grid's completion
             asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-            // layer-0 input recomputed (positional encoding), features
-            // 40..127 are zero padding so M = 128
-            float xa[32], xb[32];
+            // layer-0 input recomputed (positional encoding) by the half
+            // owning features 0..63.  A rows (fan-in) 64..127 are left as
+            // they are: row i of dW0^T depends only on A row i, and the drain
+            // stores rows i < fi0 (<= 40) only
             if (h == 0) {
+              float xa[32], xb[32];
               float x0[kK0];
               input_row(st, sCoef, gs0 + row, row < ns, x0);
 #pragma unroll
@@ -769,12 +771,9 @@ __global__ void __launch_bounds__(kTCThreads, 1)
                 xa[i] = x0[i];
                 xb[i] = (32 + i < kK0) ? x0[32 + i < kK0 ? 32 + i : 0] : 0.f;
               }
-            } else {
-#pragma unroll
-              for (int i = 0; i < 32; ++i) xa[i] = xb[i] = 0.f;
+              put_mn(xt, c0, xa);
+              put_mn(xt, c0 + 32, xb);
             }
-            put_mn(xt, c0, xa);
-            put_mn(xt, c0 + 32, xb);
           } else {
             float xv[2][32];
             ld64(R(l) + c0, R(l) + c0 + 32, xv[0], xv[1]);

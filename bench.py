@@ -527,7 +527,10 @@ def main():
                                 "kernel_ms is the branch's event span inside the step, which includes waiting "
                                 "for KF32 to free whole SMs",
                         "peak_source": tf32_src})
-        try:  # the same background stack alone on an idle GPU (prep + KT + reduce + Adam)
+        try:  # the same background stack alone on an idle GPU (prep + KT + reduce + Adam);
+            # VM_BENCH_ALONE=0 skips it (ncu launch lists: per-step kernels only)
+            if os.environ.get("VM_BENCH_ALONE", "1") == "0":
+                raise RuntimeError("skipped (VM_BENCH_ALONE=0)")
             alone = kt_alone_ms(cfg.rays_background, cfg.points_per_ray)
             kernels[-1]["alone_call_ms"] = alone
             kernels[-1]["alone_frac"] = flop_bg / (alone * 1e-3) / 1e12 / tf32_peak

@@ -12,10 +12,13 @@
 // run on CUDA cores in fp32 with the reference's operation order.
 //
 // On-chip data flow (no activation ever touches HBM):
-//  * TMEM (512 columns x 128 lanes, lane = sample row): R0 = MMA accumulator
-//    (forward pre-activations, input-gradients, weight-gradient tiles),
-//    R1..R3 = activations X1..X3 (fp32), overwritten in place by the
-//    back-propagated gradients G2..G0 once they are no longer needed.
+//  * TMEM (512 columns x 128 lanes, lane = sample row): R0 = accumulator of
+//    the forward pre-activations, the input-gradients (dx) and the output
+//    layer's dW3; R1..R3 = activations X1..X3 (fp32).  In the backward each
+//    thread keeps its row of G_l in registers, so dW_l accumulates into
+//    R(l+1) (the region X_{l+1} occupied) while dx_l accumulates into R0 on a
+//    second accumulator barrier: both GEMMs of a layer are issued back to
+//    back and dW_l drains while dx_l runs.
 //  * Shared memory: a 3-slot ring of 64 KB operand slots (A | B, each a
 //    hi/lo pair).  Forward / input-gradient GEMMs stage A = activations or
 //    gradients [128 samples][32 features] (core-matrix interleaved, K-major,
@@ -24,8 +27,8 @@
 //    L2-resident image (tc_prep_kernel builds it once per step).
 //    Weight-gradient GEMMs (K = samples, one quadrant's 32 rows per chunk)
 //    use MN-major SWIZZLE_128B_BASE32B tiles written as float4s by the
-//    sample's thread (hidden layers: dW^T = X^T G); layer 0 uses 128B-swizzled
-//    K-major transposed tiles.
+//    sample's thread (dW^T = X^T G for every layer; layer 0's fan-in rows
+//    >= 64 are not staged since only rows < fi0 are drained).
 //  * Warps 0-7 (two per TMEM lane quadrant, 64 columns each) stage, run the
 //    epilogues and the render chain; warp 8 lane 0 issues the MMAs
 //    (tcgen05.mma.cta_group::1.kind::tf32) from an smem schedule table and
@@ -750,7 +753,7 @@ __global__ void __launch_bounds__(kTCThreads, 1)
         uint8_t* sl = acquire();
         if (q == c) {
           uint8_t* gt = sl + kHalfSlot;  // B = G_l (N = fan-out)
-          uint8_t* xt = sl;              // A = X_l (M = fan-in; layer 0 zero-padded to 128)
+          uint8_t* xt = sl;              // A = X_l (M = fan-in; layer 0: rows >= 64 not staged)
           put_mn(gt, c0, gv[0]);
           put_mn(gt, c0 + 32, gv[1]);
           if (l == 0) {

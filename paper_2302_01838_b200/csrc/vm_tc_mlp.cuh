@@ -740,11 +740,11 @@ __global__ void __launch_bounds__(kTCThreads, 1)
 #pragma unroll 1
     for (int l = L - 2; l >= 0; --l) {
       // dW_l = G_l^T X_l, K = samples: chunk c = quadrant c's 32 rows, each
-      // half stages its 64 features of both operands.  Hidden layers compute
+      // half stages its 64 features of both operands.  Every layer computes
       // dW_l^T = X_l^T G_l from MN-major tiles (A = X_l, B = G_l, each thread
       // writes its own sample's features as float4s), so TMEM lane = fan-in
-      // and the drain writes whole 128-B rows of the gradient; layer 0 (fan-in
-      // 33) keeps K-major transposed tiles with A = G_0^T (M = fan-out).
+      // and the drain writes whole 128-B rows of the gradient (layer 0: the
+      // rows i < fi0 only).
       // Every thread holds its G_l row (owned columns) in registers before
       // its first release: dW_l accumulates into TMEM region l+1, and the row
       // feeds the dx_l operand and the bias gradient.
